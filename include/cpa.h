@@ -1,0 +1,174 @@
+/*
+ * cpa.h -- C ABI of libcpa.so, the B200 (sm_100a) chunked-prefill hot path of
+ * CompactAttention (arXiv 2605.16839, "Block-Union KV Selection").
+ *
+ * One chunk step = three stages (§3.1):
+ *   (1) pattern search: per (batch b, query head h, q-block i, kv-block j) block mask
+ *       M[b,h,i,j] from a max-threshold estimator over the accumulated KV cache
+ *       (keep rule SPEC.md:220-238, pooled-query variant SPEC.md:269);
+ *   (2) selection: Q-block union  Mbar[b,h,j] = OR_i M[b,h,i,j]
+ *                  intra-group union G[b,g,j] = OR_{h in H(g)} Mbar[b,h,j]
+ *                  table T[b,g] = {j | G[b,g,j] = 1} as CSR kv_indptr/kv_indices
+ *                  (PAPER.md:206, 533-534);
+ *   (3) execution: causal attention of the whole chunk over only the tabled blocks,
+ *       read in place from the paged KV cache.
+ *
+ * Conventions (all entry points):
+ *   - Host-callable, stream-ordered on `stream` (a cudaStream_t passed as void*; NULL =
+ *     legacy default stream). They never synchronize, never allocate or free device
+ *     memory and keep no pointer after they return. Re-entrant.
+ *   - Every pointer argument is a DEVICE pointer owned by the caller unless stated.
+ *   - Synchronous validation errors are returned as a cpa_status and leave every output
+ *     untouched; cpa_last_error() (thread-local) gives the detail. Asynchronous CUDA
+ *     faults surface on a later CUDA call (standard CUDA semantics).
+ *   - Inputs are bf16. Non-finite inputs are undefined behaviour.
+ *   - No CPU fallback exists: without an sm_100a device every call returns
+ *     CPA_ERR_CUDA / CPA_ERR_UNSUPPORTED.
+ *
+ * Notation: B batch, Hq query heads, Hkv KV heads,
+ *   E = exec_group_size query heads per execution group ("a KV group by default",
+ *   PAPER.md:203; 4 under sub-KV-group union), Gn = Hq/E groups,
+ *   d head_dim, bs block_size (= page size = q-block size),
+ *   C chunk_len, P prefix_len (tokens already cached; P % bs == 0), L = P + C,
+ *   nqb = ceil(C/bs), nkvb = ceil(L/bs), pb = P/bs, nwords = ceil(nkvb/32).
+ *   Query position p in [0,C) sits at absolute position P+p and may attend to
+ *   absolute positions t <= P+p.
+ */
+#ifndef CPA_H_
+#define CPA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPA_VERSION 1
+
+#if defined(__GNUC__)
+#define CPA_API __attribute__((visibility("default")))
+#else
+#define CPA_API
+#endif
+
+typedef enum {
+  CPA_OK = 0,
+  CPA_ERR_NULL = 1,        /* a required pointer is NULL */
+  CPA_ERR_SHAPE = 2,       /* Hq % Hkv, E does not divide Hq/Hkv, C < 1, nkvb > max_blocks_per_seq,
+                              B < 1 (SPEC.md:52, 134 shape errors) */
+  CPA_ERR_UNSUPPORTED = 3, /* head_dim not in {64,128}; block_size not in {16,32,64,128};
+                              no sm_100 device */
+  CPA_ERR_MISALIGNED = 4,  /* P % bs != 0 (SPEC.md:167 uniform prefix, R8);
+                              a pointer not 16-byte aligned; a stride not a multiple of 8 */
+  CPA_ERR_ALPHA = 5,       /* alpha not in (0, 1] */
+  CPA_ERR_WORKSPACE = 6,   /* ws == NULL or ws_bytes < cpa_workspace_bytes() */
+  CPA_ERR_CAPACITY = 7,    /* tables->capacity < B*Gn*nkvb */
+  CPA_ERR_CUDA = 8         /* a CUDA runtime/driver call failed (see cpa_last_error) */
+} cpa_status;
+
+/* flags */
+enum {
+  CPA_F_SINK = 1u,        /* always keep kv-block 0 (default on in the binding) */
+  CPA_F_MASK_IN = 2u,     /* skip the estimator: M is read from tables->mask_bits */
+  CPA_F_MASK_OUT = 4u,    /* also write M to tables->mask_bits */
+  CPA_F_SCORES_OUT = 8u,  /* also write block scores / row max to tables->scores / ->row_max */
+  CPA_F_OUT_F32 = 16u     /* O is fp32 instead of bf16 (parity/debug) */
+};
+
+typedef struct {
+  int32_t batch;           /* B >= 1 */
+  int32_t num_q_heads;     /* Hq (heads present in q/o for this call) */
+  int32_t num_kv_heads;    /* Hkv (heads present in the cache for this call) */
+  int32_t head_dim;        /* d in {64, 128} */
+  int32_t block_size;      /* bs in {16, 32, 64, 128}; page size == selection block size */
+  int32_t exec_group_size; /* E; 0 => Hq/Hkv. Must divide Hq/Hkv. */
+  int32_t chunk_len;       /* C >= 1; the last chunk of a prompt may be shorter */
+  int32_t prefix_len;      /* P >= 0, P % bs == 0 */
+  float alpha;             /* keep threshold in (0,1]; paper's CA-FP uses 0.06 */
+  float sm_scale;          /* logit scale; 0 => 1/sqrt(d) */
+  uint32_t flags;          /* CPA_F_* */
+  int64_t q_token_stride;  /* elements between consecutive tokens of q / o; 0 => Hq*d.
+                              Lets a rank pass a head slice of a larger [B,C,Hq_total,d] tensor. */
+} cpa_params;
+
+/* Paged KV cache (PAPER.md:237-249 KV-head-major pages).
+ * Element (physical page pg, kv head h, token slot t, dim e) of K (resp. V) lives at
+ *   k_pages + pg*page_stride + h*head_stride + t*head_dim + e      (bf16 elements)
+ * so every (page, kv head) is one contiguous [bs, d] region. A pool laid out
+ * [num_pages, Hkv, bs, d] has head_stride = bs*d, page_stride = Hkv*bs*d; the paper's
+ * per-sequence [B, Hkv, L, d] layout is page = b*nblocks + j, head_stride = L*d,
+ * page_stride = bs*d.  Logical block j of sequence b is page page_table[b*max_blocks_per_seq + j].
+ * Slots past the end of the sequence in its last page must be finite (pools are
+ * zero-initialised by the caller; SURVEY §7 hard part 7). */
+typedef struct {
+  void* k_pages;                /* bf16 (written only by cpa_append_kv / cpa_chunk_step append) */
+  void* v_pages;                /* bf16 */
+  int64_t page_stride;          /* elements; 0 => Hkv*bs*d */
+  int64_t head_stride;          /* elements; 0 => bs*d */
+  const int32_t* page_table;    /* int32 [B, max_blocks_per_seq], device */
+  int32_t max_blocks_per_seq;
+  int32_t num_pages;            /* pages addressable from k_pages / v_pages */
+} cpa_kv_cache;
+
+/* Per-chunk block tables (CSR over pseudo-rows r = b*Gn + g).
+ * kv_indices holds LOGICAL block ids j, ascending within a row; the chunk blocks [pb, nkvb)
+ * are always present (fully-open current chunk), so no row is empty. */
+typedef struct {
+  int32_t* kv_indptr;    /* int32 [B*Gn + 1] (out of cpa_build_tables, in of cpa_paged_attention) */
+  int32_t* kv_indices;   /* int32 [capacity] */
+  int64_t capacity;      /* >= B*Gn*nkvb */
+  uint32_t* mask_bits;   /* optional u32 [B, Hq, nqb, nwords]; bit (j%32) of word j/32 is M[b,h,i,j].
+                            Input with CPA_F_MASK_IN, output with CPA_F_MASK_OUT. */
+  float* scores;         /* optional fp32 [B, Gn, nkvb, Rpad] (CPA_F_SCORES_OUT): block score
+                            m[b, g*E + r/nqb, r%nqb, j] at row r < E*nqb; -inf where j > pb + i.
+                            Rpad = 128*ceil(E*nqb/128). */
+  float* row_max;        /* optional fp32 [B, Gn, Rpad] (CPA_F_SCORES_OUT): m*[b,h,i] = max_j m */
+  int32_t* dev_status;   /* optional int32[1]: with CPA_F_MASK_IN, set to 1 + r for a row r whose
+                            mask lacks a chunk block (open-chunk violation); 0 otherwise */
+} cpa_tables;
+
+/* Device workspace needed by cpa_build_tables / cpa_paged_attention / cpa_chunk_step. */
+CPA_API size_t cpa_workspace_bytes(const cpa_params* p);
+
+/* Stages (1)+(2): estimator -> M -> Q-block union -> intra-group union -> CSR tables.
+ *   q:     bf16 [B, C, Hq, d] (token stride p->q_token_stride), the chunk's queries.
+ *   cache: K pages must already contain tokens [0, L) of every sequence.
+ *   out:   kv_indptr / kv_indices written (plus mask_bits / scores per flags).
+ * Estimator: qbar[b,h,i] = mean of the valid queries of q-block i;
+ *   m[b,h,i,j] = max over keys t of block j with t <= P + last query of block i of
+ *   sm_scale * qbar . k_t;  m* = max_j m;  M = causal && (m - m* >= ln(alpha) ||
+ *   j >= pb || (SINK && j == 0)). */
+CPA_API int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
+                     cpa_tables* out, void* ws, size_t ws_bytes, void* stream);
+
+/* Stage (3): O[b,p,h] = sum_{t in A(p)} softmax_t(sm_scale q_p . k_t) v_t with
+ *   A(p) = { t : floor(t/bs) in T[b, h/E], t <= P + p }  (absolute coordinates).
+ *   tables == NULL => dense causal chunk attention over every block [0, nkvb) (the baseline).
+ *   o: bf16 (or fp32 with CPA_F_OUT_F32) [B, C, Hq, d], token stride p->q_token_stride. */
+CPA_API int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
+                        const cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
+                        void* stream);
+
+/* One whole chunk step: optional append of the chunk's K/V into the pages
+ * (k_chunk/v_chunk bf16 [B, C, Hkv, d], token slots [P, P+C); NULL => already resident),
+ * then cpa_build_tables, then cpa_paged_attention over the built tables. */
+CPA_API int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                   const cpa_kv_cache* cache, cpa_tables* tables, void* o, void* ws,
+                   size_t ws_bytes, void* stream);
+
+/* Append only (SPEC.md:130-138 append_chunk): write k_chunk/v_chunk [B, C, Hkv, d] into
+ * token slots [P, P+C) of each sequence's pages. K/V pools are written in place. */
+CPA_API int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk,
+                  const cpa_kv_cache* cache, void* stream);
+
+CPA_API const char* cpa_status_string(int status);
+CPA_API const char* cpa_last_error(void);  /* thread-local detail of the last failing call */
+CPA_API int cpa_version(void);
+/* Number of kernels the last successful call on this thread enqueued (for bench accounting). */
+CPA_API int cpa_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPA_H_ */

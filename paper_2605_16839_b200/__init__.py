@@ -1,0 +1,219 @@
+"""paper_2605_16839_b200 -- B200-native CompactAttention chunked-prefill hot path.
+
+Thin Python binding over libcpa.so (include/cpa.h). Argument marshalling only: every step of
+the path (estimator, masks, unions, CSR tables, paged attention, append) runs in the sm_100a
+kernels of csrc/. PyTorch supplies device memory and streams. There is no CPU fallback: if the
+native library is missing or the device is not sm_100 every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+__all__ = [
+    "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
+    "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
+    "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "EXPORTED_SYMBOLS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcpa.so")
+
+F_SINK, F_MASK_IN, F_MASK_OUT, F_SCORES_OUT, F_OUT_F32 = 1, 2, 4, 8, 16
+STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA_ERR_MISALIGNED",
+          "CPA_ERR_ALPHA", "CPA_ERR_WORKSPACE", "CPA_ERR_CAPACITY", "CPA_ERR_CUDA"]
+EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",
+                    "cpa_append_kv", "cpa_status_string", "cpa_last_error", "cpa_version",
+                    "cpa_last_launch_count"]
+
+
+class CpaError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        name = STATUS[status] if 0 <= status < len(STATUS) else str(status)
+        super().__init__(f"{name}: {detail}")
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("block_size", ctypes.c_int32), ("exec_group_size", ctypes.c_int32),
+                ("chunk_len", ctypes.c_int32), ("prefix_len", ctypes.c_int32), ("alpha", ctypes.c_float),
+                ("sm_scale", ctypes.c_float), ("flags", ctypes.c_uint32), ("q_token_stride", ctypes.c_int64)]
+
+
+class _Cache(ctypes.Structure):
+    _fields_ = [("k_pages", ctypes.c_void_p), ("v_pages", ctypes.c_void_p), ("page_stride", ctypes.c_int64),
+                ("head_stride", ctypes.c_int64), ("page_table", ctypes.c_void_p),
+                ("max_blocks_per_seq", ctypes.c_int32), ("num_pages", ctypes.c_int32)]
+
+
+class _Tables(ctypes.Structure):
+    _fields_ = [("kv_indptr", ctypes.c_void_p), ("kv_indices", ctypes.c_void_p), ("capacity", ctypes.c_int64),
+                ("mask_bits", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("row_max", ctypes.c_void_p),
+                ("dev_status", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcpa.so (in-tree). Raises if it is missing -- there is no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"native library {LIB_PATH} is missing; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32 = ctypes.c_void_p, ctypes.c_int
+        L.cpa_workspace_bytes.argtypes = [ctypes.POINTER(Params)]
+        L.cpa_workspace_bytes.restype = ctypes.c_size_t
+        L.cpa_build_tables.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache), ctypes.POINTER(_Tables),
+                                       vp, ctypes.c_size_t, vp]
+        L.cpa_paged_attention.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache),
+                                          ctypes.POINTER(_Tables), vp, vp, ctypes.c_size_t, vp]
+        L.cpa_chunk_step.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(_Cache),
+                                     ctypes.POINTER(_Tables), vp, vp, ctypes.c_size_t, vp]
+        L.cpa_append_kv.argtypes = [ctypes.POINTER(Params), vp, vp, ctypes.POINTER(_Cache), vp]
+        for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv):
+            f.restype = i32
+        L.cpa_status_string.argtypes = [i32]
+        L.cpa_status_string.restype = ctypes.c_char_p
+        L.cpa_last_error.restype = ctypes.c_char_p
+        L.cpa_version.restype = i32
+        L.cpa_last_launch_count.restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise CpaError(status, lib().cpa_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def make_params(batch: int, num_q_heads: int, num_kv_heads: int, head_dim: int, block_size: int,
+                chunk_len: int, prefix_len: int, alpha: float = 0.06, exec_group_size: int = 0,
+                sink: bool = True, flags: int = 0, sm_scale: float = 0.0, q_token_stride: int = 0) -> Params:
+    return Params(batch, num_q_heads, num_kv_heads, head_dim, block_size, exec_group_size, chunk_len,
+                  prefix_len, alpha, sm_scale, flags | (F_SINK if sink else 0), q_token_stride)
+
+
+def geometry(p: Params):
+    """(nqb, nkvb, pb, Gn, nwords, Rpad) -- plain integer bookkeeping from the header's notation."""
+    bs = p.block_size
+    E = p.exec_group_size or p.num_q_heads // p.num_kv_heads
+    nqb = -(-p.chunk_len // bs)
+    nkvb = -(-(p.prefix_len + p.chunk_len) // bs)
+    Gn = p.num_q_heads // E
+    return nqb, nkvb, p.prefix_len // bs, Gn, -(-nkvb // 32), 128 * (-(-(E * nqb) // 128))
+
+
+def workspace_bytes(p: Params) -> int:
+    return int(lib().cpa_workspace_bytes(ctypes.byref(p)))
+
+
+@dataclass
+class PagedKVCache:
+    """K/V page pools (bf16, each (page, kv head) a contiguous [bs, d] region) + int32 page table
+    [B, max_blocks_per_seq]. Strides are in elements (0 => pool laid out [pages, Hkv, bs, d])."""
+    k_pages: torch.Tensor
+    v_pages: torch.Tensor
+    page_table: torch.Tensor
+    page_stride: int = 0
+    head_stride: int = 0
+
+    def _c(self) -> _Cache:
+        assert self.k_pages.dtype == torch.bfloat16 and self.v_pages.dtype == torch.bfloat16
+        assert self.page_table.dtype == torch.int32 and self.page_table.is_contiguous()
+        num_pages = self.k_pages.shape[0]
+        return _Cache(_ptr(self.k_pages), _ptr(self.v_pages), self.page_stride, self.head_stride,
+                      _ptr(self.page_table), self.page_table.shape[-1], num_pages)
+
+
+@dataclass
+class BlockTables:
+    """CSR block tables T[b,g] + optional debug outputs."""
+    kv_indptr: torch.Tensor
+    kv_indices: torch.Tensor
+    mask_bits: Optional[torch.Tensor] = None
+    scores: Optional[torch.Tensor] = None
+    row_max: Optional[torch.Tensor] = None
+    dev_status: Optional[torch.Tensor] = None
+
+    def _c(self) -> _Tables:
+        return _Tables(_ptr(self.kv_indptr), _ptr(self.kv_indices), self.kv_indices.numel(),
+                       _ptr(self.mask_bits), _ptr(self.scores), _ptr(self.row_max), _ptr(self.dev_status))
+
+
+def alloc_tables(p: Params, device="cuda", mask: bool = False, scores: bool = False,
+                 status: bool = False) -> BlockTables:
+    nqb, nkvb, pb, Gn, nwords, Rpad = geometry(p)
+    B = p.batch
+    t = BlockTables(torch.empty(B * Gn + 1, dtype=torch.int32, device=device),
+                    torch.empty(B * Gn * nkvb, dtype=torch.int32, device=device))
+    if mask:
+        t.mask_bits = torch.zeros(B, p.num_q_heads, nqb, nwords, dtype=torch.int32, device=device)
+    if scores:
+        t.scores = torch.empty(B, Gn, nkvb, Rpad, dtype=torch.float32, device=device)
+        t.row_max = torch.empty(B, Gn, Rpad, dtype=torch.float32, device=device)
+    if status:
+        t.dev_status = torch.zeros(1, dtype=torch.int32, device=device)
+    return t
+
+
+def _ws(p: Params, workspace: Optional[torch.Tensor], device) -> torch.Tensor:
+    need = workspace_bytes(p)
+    if workspace is None:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+    return workspace
+
+
+def build_tables(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables,
+                 workspace: Optional[torch.Tensor] = None, stream=None) -> BlockTables:
+    ws = _ws(p, workspace, q.device if q is not None else cache.k_pages.device)
+    c, t = cache._c(), tables._c()
+    _check(lib().cpa_build_tables(ctypes.byref(p), _ptr(q), ctypes.byref(c), ctypes.byref(t),
+                                  _ptr(ws), ws.numel(), _stream(stream)))
+    return tables
+
+
+def paged_attention(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: Optional[BlockTables],
+                    out: torch.Tensor, workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    ws = _ws(p, workspace, q.device)
+    c = cache._c()
+    t = tables._c() if tables is not None else None
+    _check(lib().cpa_paged_attention(ctypes.byref(p), _ptr(q), ctypes.byref(c),
+                                     ctypes.byref(t) if t is not None else None, _ptr(out), _ptr(ws),
+                                     ws.numel(), _stream(stream)))
+    return out
+
+
+def chunk_step(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables, out: torch.Tensor,
+               k_chunk: Optional[torch.Tensor] = None, v_chunk: Optional[torch.Tensor] = None,
+               workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    ws = _ws(p, workspace, q.device)
+    c, t = cache._c(), tables._c()
+    _check(lib().cpa_chunk_step(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
+                                ctypes.byref(t), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def append_kv(p: Params, k_chunk: torch.Tensor, v_chunk: torch.Tensor, cache: PagedKVCache, stream=None):
+    c = cache._c()
+    _check(lib().cpa_append_kv(ctypes.byref(p), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c), _stream(stream)))
+
+
+def last_launch_count() -> int:
+    return int(lib().cpa_last_launch_count())

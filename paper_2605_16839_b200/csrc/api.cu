@@ -1,0 +1,381 @@
+// api.cu -- the C ABI of libcpa.so (include/cpa.h): validation, workspace carving, TMA tensor
+// maps and the stream-ordered kernel sequence of one CompactAttention chunk step.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "../../include/cpa.h"
+#include "common.cuh"
+#include "geo.cuh"
+
+namespace cpa {
+cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
+                          cudaStream_t st, int* launches);
+cudaError_t launch_block_scores(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
+                                const Geo& g, float* scores, int* mstar_key, int num_sms,
+                                cudaStream_t st, int* launches);
+cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& g,
+                          const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
+                          int* dev_status, int32_t* indptr, int32_t* indices, cudaStream_t st,
+                          int* launches);
+struct AttnArgs {
+  const int32_t* page_table;
+  const int32_t* indptr;
+  const int32_t* indices;
+  void* out;
+  int out_f32;
+};
+cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                                   const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
+cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g,
+                          long long page_stride, long long head_stride, cudaStream_t st, int* launches);
+cudaError_t launch_row_max(const int* mstar_key, const Geo& g, float* row_max, cudaStream_t st,
+                           int* launches);
+}  // namespace cpa
+
+using namespace cpa;
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+int fail(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(CPA_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- device properties
+struct DevInfo {
+  int ok = -1;  // -1 unknown, 0 unsupported, 1 sm_100
+  int num_sms = 0;
+};
+DevInfo g_dev[64];
+std::mutex g_dev_mu;
+
+int device_info(int* num_sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) return fail(CPA_ERR_UNSUPPORTED, "device index %d", dev);
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  DevInfo& d = g_dev[dev];
+  if (d.ok < 0) {
+    int major = 0, minor = 0, sms = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    d.ok = (major == 10 && minor == 0) ? 1 : 0;
+    d.num_sms = sms;
+  }
+  if (!d.ok) return fail(CPA_ERR_UNSUPPORTED, "libcpa needs an sm_100 (B200) device");
+  *num_sms = d.num_sms;
+  return CPA_OK;
+}
+
+// ---------------------------------------------------------------- TMA tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims,
+             const cuuint64_t* strides_bytes, const cuuint32_t* box, const char* what) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(CPA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), dims, strides_bytes,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CPA_ERR_CUDA, "cuTensorMapEncodeTiled(%s) failed: %d", what, (int)r);
+  return CPA_OK;
+}
+
+// ---------------------------------------------------------------- validation -> Geo
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int make_geo(const cpa_params* p, Geo* g) {
+  if (!p) return fail(CPA_ERR_NULL, "params is NULL");
+  if (p->batch < 1 || p->num_q_heads < 1 || p->num_kv_heads < 1 || p->chunk_len < 1 || p->prefix_len < 0)
+    return fail(CPA_ERR_SHAPE, "batch/heads/chunk_len must be >= 1 and prefix_len >= 0");
+  if (p->num_q_heads % p->num_kv_heads)
+    return fail(CPA_ERR_SHAPE, "num_q_heads %% num_kv_heads != 0");
+  const int kvq = p->num_q_heads / p->num_kv_heads;
+  const int E = p->exec_group_size ? p->exec_group_size : kvq;
+  if (E < 1 || kvq % E) return fail(CPA_ERR_SHAPE, "exec_group_size must divide Hq/Hkv");
+  if (p->head_dim != 64 && p->head_dim != 128) return fail(CPA_ERR_UNSUPPORTED, "head_dim must be 64 or 128");
+  const int bs = p->block_size;
+  if (bs != 16 && bs != 32 && bs != 64 && bs != 128)
+    return fail(CPA_ERR_UNSUPPORTED, "block_size must be 16, 32, 64 or 128");
+  if (p->prefix_len % bs) return fail(CPA_ERR_MISALIGNED, "prefix_len %% block_size != 0");
+  if (!(p->alpha > 0.f && p->alpha <= 1.f)) return fail(CPA_ERR_ALPHA, "alpha must be in (0, 1]");
+  const long long qs = p->q_token_stride ? p->q_token_stride : (long long)p->num_q_heads * p->head_dim;
+  if (qs < (long long)p->num_q_heads * p->head_dim || qs % 8)
+    return fail(CPA_ERR_MISALIGNED, "q_token_stride must be >= Hq*d and a multiple of 8");
+  g->B = p->batch;
+  g->Hq = p->num_q_heads;
+  g->Hkv = p->num_kv_heads;
+  g->d = p->head_dim;
+  g->bs = bs;
+  g->E = E;
+  g->Gn = p->num_q_heads / E;
+  g->C = p->chunk_len;
+  g->P = p->prefix_len;
+  g->L = g->P + g->C;
+  g->nqb = (g->C + bs - 1) / bs;
+  g->nkvb = (g->L + bs - 1) / bs;
+  g->pb = g->P / bs;
+  g->nwords = (g->nkvb + 31) / 32;
+  g->R = E * g->nqb;
+  g->Rpad = ((g->R + 127) / 128) * 128;
+  g->maxb = 0;
+  g->kv_per_q = kvq;
+  g->scale = p->sm_scale > 0.f ? p->sm_scale : 1.0f / sqrtf((float)p->head_dim);
+  g->ln_alpha = logf(p->alpha);
+  g->flags = p->flags;
+  g->q_stride = qs;
+  return CPA_OK;
+}
+
+int check_cache(const cpa_kv_cache* c, Geo* g, long long* ps, long long* hs) {
+  if (!c || !c->k_pages || !c->v_pages || !c->page_table) return fail(CPA_ERR_NULL, "cache pointers");
+  if (!aligned16(c->k_pages) || !aligned16(c->v_pages)) return fail(CPA_ERR_MISALIGNED, "pages not 16B aligned");
+  if (c->max_blocks_per_seq < g->nkvb)
+    return fail(CPA_ERR_SHAPE, "max_blocks_per_seq %d < nkvb %d", c->max_blocks_per_seq, g->nkvb);
+  if (c->num_pages < 1) return fail(CPA_ERR_SHAPE, "num_pages < 1");
+  *hs = c->head_stride ? c->head_stride : (long long)g->bs * g->d;
+  *ps = c->page_stride ? c->page_stride : (long long)g->Hkv * g->bs * g->d;
+  if (*hs % 8 || *ps % 8) return fail(CPA_ERR_MISALIGNED, "page/head strides must be multiples of 8");
+  g->maxb = c->max_blocks_per_seq;
+  return CPA_OK;
+}
+
+// workspace carve-up
+struct WS {
+  __nv_bfloat16* qbar;
+  float* scores;
+  int* mstar_key;
+  uint32_t* gwords;
+  size_t total;
+};
+size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+WS carve(const Geo& g, void* base) {
+  WS w;
+  const uintptr_t p = reinterpret_cast<uintptr_t>(base);
+  size_t off = 0;
+  w.qbar = reinterpret_cast<__nv_bfloat16*>(p + off);
+  off += up256((size_t)2 * g.B * g.Gn * g.Rpad * g.d * 2);
+  w.scores = reinterpret_cast<float*>(p + off);
+  off += up256((size_t)g.B * g.Gn * g.nkvb * g.Rpad * 4);
+  w.mstar_key = reinterpret_cast<int*>(p + off);
+  off += up256((size_t)g.B * g.Gn * g.Rpad * 4);
+  w.gwords = reinterpret_cast<uint32_t*>(p + off);
+  off += up256((size_t)g.B * g.Gn * g.nwords * 4);
+  w.total = off;
+  return w;
+}
+
+int q_map(CUtensorMap* m, const void* q, const Geo& g) {
+  cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.Hq, (cuuint64_t)g.C, (cuuint64_t)g.B};
+  cuuint64_t str[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.q_stride * 2, (cuuint64_t)g.C * g.q_stride * 2};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  return make_map(m, q, 4, dims, str, box, "q");
+}
+int kv_map(CUtensorMap* m, const void* pages, const Geo& g, int num_pages, long long ps, long long hs,
+           const char* what) {
+  cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.bs, (cuuint64_t)g.Hkv, (cuuint64_t)num_pages};
+  cuuint64_t str[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)hs * 2, (cuuint64_t)ps * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)g.bs, 1, 1};
+  return make_map(m, pages, 4, dims, str, box, what);
+}
+
+int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c,
+                      long long ps, long long hs, cpa_tables* out, void* ws, size_t ws_bytes,
+                      cudaStream_t st, int num_sms) {
+  if (!out || !out->kv_indptr || !out->kv_indices) return fail(CPA_ERR_NULL, "tables pointers");
+  if (out->capacity < (long long)g.B * g.Gn * g.nkvb)
+    return fail(CPA_ERR_CAPACITY, "capacity %lld < B*Gn*nkvb = %lld", (long long)out->capacity,
+                (long long)g.B * g.Gn * g.nkvb);
+  const bool mask_in = (p->flags & CPA_F_MASK_IN) != 0;
+  if (mask_in && !out->mask_bits) return fail(CPA_ERR_NULL, "CPA_F_MASK_IN needs tables->mask_bits");
+  if ((p->flags & CPA_F_MASK_OUT) && !out->mask_bits) return fail(CPA_ERR_NULL, "CPA_F_MASK_OUT needs mask_bits");
+  if ((p->flags & CPA_F_SCORES_OUT) && (!out->scores || !out->row_max))
+    return fail(CPA_ERR_NULL, "CPA_F_SCORES_OUT needs scores and row_max");
+  WS w = carve(g, ws);
+  if (!ws || ws_bytes < w.total) return fail(CPA_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.total);
+  cudaError_t e;
+  int* launches = &g_launches;
+  float* scores = (p->flags & CPA_F_SCORES_OUT) ? out->scores : w.scores;
+  if (!mask_in) {
+    if (!q) return fail(CPA_ERR_NULL, "q is NULL");
+    if (!aligned16(q)) return fail(CPA_ERR_MISALIGNED, "q not 16B aligned");
+    CUtensorMap tq, tk;
+    cuuint64_t dims[2] = {(cuuint64_t)g.d, (cuuint64_t)2 * g.B * g.Gn * g.Rpad};
+    cuuint64_t str[1] = {(cuuint64_t)g.d * 2};
+    cuuint32_t box[2] = {64, 128};
+    int s;
+    if ((s = make_map(&tq, w.qbar, 2, dims, str, box, "qbar")) != CPA_OK) return s;
+    if ((s = kv_map(&tk, c->k_pages, g, c->num_pages, ps, hs, "k")) != CPA_OK) return s;
+    if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(q), g, w.qbar, w.mstar_key, st, launches)) != cudaSuccess)
+      return cuda_fail(e, "pool_q");
+    if ((e = launch_block_scores(tq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) != cudaSuccess)
+      return cuda_fail(e, "block_scores");
+    if (p->flags & CPA_F_SCORES_OUT) {
+      if ((e = launch_row_max(w.mstar_key, g, out->row_max, st, launches)) != cudaSuccess)
+        return cuda_fail(e, "row_max");
+    }
+  }
+  if (mask_in && out->dev_status) {
+    if ((e = cudaMemsetAsync(out->dev_status, 0, sizeof(int), st)) != cudaSuccess) return cuda_fail(e, "memset");
+  }
+  e = launch_tables(scores, w.mstar_key, g, mask_in ? out->mask_bits : nullptr,
+                    (!mask_in && (p->flags & CPA_F_MASK_OUT)) ? out->mask_bits : nullptr, w.gwords,
+                    mask_in ? out->dev_status : nullptr, out->kv_indptr, out->kv_indices, st, launches);
+  if (e != cudaSuccess) return cuda_fail(e, "tables");
+  return CPA_OK;
+}
+
+int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
+                   long long hs, const cpa_tables* t, void* o, cudaStream_t st) {
+  if (!q || !o) return fail(CPA_ERR_NULL, "q/o is NULL");
+  if (!aligned16(q) || !aligned16(o)) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
+  if (t && (!t->kv_indptr || !t->kv_indices)) return fail(CPA_ERR_NULL, "tables pointers");
+  CUtensorMap tq, tk, tv;
+  int s;
+  if ((s = q_map(&tq, q, g)) != CPA_OK) return s;
+  if ((s = kv_map(&tk, c->k_pages, g, c->num_pages, ps, hs, "k")) != CPA_OK) return s;
+  if ((s = kv_map(&tv, c->v_pages, g, c->num_pages, ps, hs, "v")) != CPA_OK) return s;
+  AttnArgs a;
+  a.page_table = c->page_table;
+  a.indptr = t ? t->kv_indptr : nullptr;
+  a.indices = t ? t->kv_indices : nullptr;
+  a.out = o;
+  a.out_f32 = (p->flags & CPA_F_OUT_F32) ? 1 : 0;
+  cudaError_t e = launch_paged_attention(tq, tk, tv, g, a, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "paged_attention");
+  return CPA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t cpa_workspace_bytes(const cpa_params* p) {
+  Geo g;
+  if (make_geo(p, &g) != CPA_OK) return 0;
+  return carve(g, nullptr).total;
+}
+
+int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_cache* cache, cpa_tables* out,
+                     void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  return build_tables_impl(p, g, q, cache, ps, hs, out, ws, ws_bytes, (cudaStream_t)stream, sms);
+}
+
+int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache, const cpa_tables* tables,
+                        void* o, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  return attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream);
+}
+
+int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk, const cpa_kv_cache* cache,
+                  void* stream) {
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  if (!k_chunk || !v_chunk) return fail(CPA_ERR_NULL, "k_chunk/v_chunk NULL");
+  if (!aligned16(k_chunk) || !aligned16(v_chunk)) return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
+  cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, (cudaStream_t)stream, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "append");
+  return CPA_OK;
+}
+
+int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                   const cpa_kv_cache* cache, cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
+                   void* stream) {
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  if ((k_chunk == nullptr) != (v_chunk == nullptr)) return fail(CPA_ERR_NULL, "k_chunk/v_chunk: both or neither");
+  if (!q || !o) return fail(CPA_ERR_NULL, "q/o is NULL");
+  if (!tables) return fail(CPA_ERR_NULL, "tables is NULL");
+  int total = 0;
+  if (k_chunk) {
+    if (!aligned16(k_chunk) || !aligned16(v_chunk)) return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
+    cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, (cudaStream_t)stream, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "append");
+  }
+  total += g_launches;
+  g_launches = 0;
+  if ((s = build_tables_impl(p, g, q, cache, ps, hs, tables, ws, ws_bytes, (cudaStream_t)stream, sms)) != CPA_OK)
+    return s;
+  total += g_launches;
+  g_launches = 0;
+  if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream)) != CPA_OK) return s;
+  g_launches += total;
+  return CPA_OK;
+}
+
+const char* cpa_status_string(int status) {
+  switch (status) {
+    case CPA_OK: return "CPA_OK";
+    case CPA_ERR_NULL: return "CPA_ERR_NULL";
+    case CPA_ERR_SHAPE: return "CPA_ERR_SHAPE";
+    case CPA_ERR_UNSUPPORTED: return "CPA_ERR_UNSUPPORTED";
+    case CPA_ERR_MISALIGNED: return "CPA_ERR_MISALIGNED";
+    case CPA_ERR_ALPHA: return "CPA_ERR_ALPHA";
+    case CPA_ERR_WORKSPACE: return "CPA_ERR_WORKSPACE";
+    case CPA_ERR_CAPACITY: return "CPA_ERR_CAPACITY";
+    case CPA_ERR_CUDA: return "CPA_ERR_CUDA";
+    default: return "CPA_ERR_UNKNOWN";
+  }
+}
+const char* cpa_last_error(void) { return g_err; }
+int cpa_version(void) { return CPA_VERSION; }
+int cpa_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+// estimator.cu -- §8 rows a1/a2: pooled-query max-threshold block scores on sm_100a.
+//
+// SPEC.md:220-228 + 269 (pooled variant): for each (b, h, q-block i) the block-mean query
+// qbar; for each KV block j <= pb+i the tile max over its causal keys of scale*qbar.k_t.
+// One execution group (b, g) is one GEMM: A = qbar rows r = hl*nqb + i (E*nqb rows, padded
+// to 128), B = each K page of KV head g*E/(Hq/Hkv) streamed by TMA through the page table;
+// D = 128 x bs fp32 in TMEM; the epilogue takes the per-row max over the page's keys.
+// qbar is split hi = bf16(qbar), lo = bf16(qbar - hi) and both are accumulated into the same
+// TMEM tile, so the score carries ~2^-16 relative error instead of bf16's 2^-8 (K2).
+#include "common.cuh"
+#include "geo.cuh"
+
+namespace cpa {
+
+// ---------------------------------------------------------------- a1: pool Q
+// grid (nqb, Hq, B), block d threads. qbar: [2][B*Gn*Rpad][d] bf16 (hi rows, then lo rows).
+__global__ void k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
+                         __nv_bfloat16* __restrict__ qbar, int* __restrict__ mstar_key) {
+  const int i = blockIdx.x, h = blockIdx.y, b = blockIdx.z, e = threadIdx.x;
+  const int p0 = i * g.bs, p1 = min(p0 + g.bs, g.C);
+  const __nv_bfloat16* src = q + ((long long)b * g.C + p0) * g.q_stride + (long long)h * g.d + e;
+  float acc = 0.f;
+  for (int p = p0; p < p1; ++p, src += g.q_stride) acc += __bfloat162float(*src);
+  const float mean = acc / float(p1 - p0);
+  const __nv_bfloat16 hi = __float2bfloat16_rn(mean);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(mean - __bfloat162float(hi));
+  const int grp = h / g.E, hl = h % g.E;
+  const long long row = ((long long)b * g.Gn + grp) * g.Rpad + hl * g.nqb + i;
+  const long long nrows = (long long)g.B * g.Gn * g.Rpad;
+  qbar[row * g.d + e] = hi;
+  qbar[(nrows + row) * g.d + e] = lo;
+  if (e == 0) mstar_key[row] = float_key(-INFINITY);
+}
+
+// zero the padding rows r in [R, Rpad) of qbar (keeps the padded MMA rows finite)
+__global__ void k_pool_pad(Geo g, __nv_bfloat16* __restrict__ qbar) {
+  const long long nrows = (long long)g.B * g.Gn * g.Rpad;
+  const int npad = g.Rpad - g.R;
+  const long long total = (long long)g.B * g.Gn * npad * g.d;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
+       x += (long long)gridDim.x * blockDim.x) {
+    const long long e = x % g.d, t = x / g.d;
+    const long long bg = t / npad, r = g.R + t % npad;
+    const long long row = bg * g.Rpad + r;
+    qbar[row * g.d + e] = __float2bfloat16_rn(0.f);
+    qbar[(nrows + row) * g.d + e] = __float2bfloat16_rn(0.f);
+  }
+}
+
+// ---------------------------------------------------------------- a2: block scores
+template <int D, int BS>
+struct ScoreCfg {
+  static constexpr int kAtoms = D / 64;            // 128-byte swizzle atoms along d
+  static constexpr int kStages = 4;
+  static constexpr int kABytes = 128 * D * 2;      // one 128-row qbar tile
+  static constexpr int kKBytes = BS * D * 2;       // one K page
+  static constexpr int kTmemCols = (2 * BS) <= 32 ? 32 : (2 * BS);
+  static constexpr int kSmem = 2 * kABytes + kStages * kKBytes + 1024 /*align*/ + 256 /*bars*/;
+};
+
+template <int D, int BS>
+__global__ void __launch_bounds__(192, 1)
+    k_block_scores(const __grid_constant__ CUtensorMap tm_qbar, const __grid_constant__ CUtensorMap tm_k,
+                   const int32_t* __restrict__ page_table, Geo g, int pages_per_cta,
+                   float* __restrict__ scores, int* __restrict__ mstar_key) {
+  using Cfg = ScoreCfg<D, BS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA_hi = smem;
+  uint8_t* sA_lo = smem + Cfg::kABytes;
+  uint8_t* sK = smem + 2 * Cfg::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sK + Cfg::kStages * Cfg::kKBytes);
+  uint64_t* bar_a = bars;                          // A tiles landed
+  uint64_t* full = bars + 1;                       // [kStages] K page landed
+  uint64_t* empty = full + Cfg::kStages;           // [kStages] K page consumed
+  uint64_t* acc_full = empty + Cfg::kStages;       // [2] accumulator ready
+  uint64_t* acc_empty = acc_full + 2;              // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int bg = blockIdx.z, b = bg / g.Gn, grp = bg % g.Gn;
+  const int rt = blockIdx.y;
+  const int j0 = blockIdx.x * pages_per_cta;
+  const int j1 = min(g.nkvb, j0 + pages_per_cta);
+  const int n_pages = j1 - j0;
+  if (n_pages <= 0) return;  // uniform across the CTA
+  const int kvh = group_kv_head(g, grp);
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_qbar);
+    tma_prefetch_desc(&tm_k);
+    mbar_init(bar_a, 1);
+    for (int s = 0; s < Cfg::kStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(acc_full + s, 1); mbar_init(acc_empty + s, 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      const int row0 = bg * g.Rpad + rt * 128;
+      const int nrows = g.B * g.Gn * g.Rpad;
+      mbar_expect_tx(bar_a, 2 * Cfg::kABytes);
+#pragma unroll
+      for (int a = 0; a < Cfg::kAtoms; ++a) {
+        tma_load_2d(sA_hi + a * 128 * 128, &tm_qbar, bar_a, 64 * a, row0);
+        tma_load_2d(sA_lo + a * 128 * 128, &tm_qbar, bar_a, 64 * a, nrows + row0);
+      }
+      const uint64_t pol = l2_policy_evict_first();
+      for (int n = 0; n < n_pages; ++n) {
+        const int s = n % Cfg::kStages;
+        mbar_wait(empty + s, ((n / Cfg::kStages) & 1) ^ 1);
+        const int page = __ldg(page_table + (long long)b * g.maxb + j0 + n);
+        uint8_t* dst = sK + s * Cfg::kKBytes;
+        mbar_expect_tx(full + s, Cfg::kKBytes);
+#pragma unroll
+        for (int a = 0; a < Cfg::kAtoms; ++a)
+          tma_load_4d_hint(dst + a * BS * 128, &tm_k, full + s, 64 * a, 0, kvh, page, pol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BS, 0, 0);
+      mbar_wait(bar_a, 0);
+      tc_fence_after();
+      const uint32_t a_hi = smem_u32(sA_hi), a_lo = smem_u32(sA_lo);
+      for (int n = 0; n < n_pages; ++n) {
+        const int s = n % Cfg::kStages, acc = n & 1;
+        mbar_wait(full + s, (n / Cfg::kStages) & 1);
+        mbar_wait(acc_empty + acc, ((n >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(sK + s * Cfg::kKBytes);
+        const uint32_t d_tm = tmem + acc * BS;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const uint32_t abase = half ? a_lo : a_hi;
+#pragma unroll
+          for (int a = 0; a < Cfg::kAtoms; ++a)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t ad = umma_desc_sw128(abase + a * 128 * 128 + kk * 32, 16, 1024);
+              const uint64_t bd = umma_desc_sw128(kb + a * BS * 128 + kk * 32, 16, 1024);
+              mma_ss(d_tm, ad, bd, idesc, (half | a | kk) != 0);
+            }
+        }
+        tc_commit(empty + s);
+        tc_commit(acc_full + acc);
+      }
+    }
+  } else {  // ---------------- epilogue: warps 2..5, one accumulator row per thread
+    const int quarter = warp & 3;
+    const int r_loc = quarter * 32 + lane;
+    const int r = rt * 128 + r_loc;
+    const bool valid_row = r < g.R;
+    const int i = valid_row ? r % g.nqb : 0;
+    const int lim = g.P + min((i + 1) * g.bs, g.C) - 1;  // last absolute key the pooled query sees
+    float row_best = -INFINITY;
+    for (int n = 0; n < n_pages; ++n) {
+      const int acc = n & 1, j = j0 + n;
+      mbar_wait(acc_full + acc, (n >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BS;
+      float mx = -INFINITY;
+      const int tbase = j * g.bs;
+      const bool needs_mask = tbase + BS - 1 > lim;
+      if constexpr (BS >= 32) {
+#pragma unroll
+        for (int c0 = 0; c0 < BS; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c0, v);
+          tmem_wait_ld();
+          if (needs_mask) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (tbase + c0 + c <= lim) mx = fmaxf(mx, __uint_as_float(v[c]));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(v[c]));
+          }
+        }
+      } else {
+        uint32_t v[16];
+        tmem_ld16(taddr, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < BS && tbase + c <= lim) mx = fmaxf(mx, __uint_as_float(v[c]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + acc);
+      const bool causal = valid_row && j <= g.pb + i;
+      const float m = causal ? mx * g.scale : -INFINITY;
+      scores[((long long)bg * g.nkvb + j) * g.Rpad + r] = m;
+      row_best = fmaxf(row_best, m);
+    }
+    if (valid_row) atomicMax(mstar_key + (long long)bg * g.Rpad + r, float_key(row_best));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+int score_smem_bytes(int d, int bs) {
+#define CPA_SC(DD, BB) if (d == DD && bs == BB) return ScoreCfg<DD, BB>::kSmem;
+  CPA_SC(64, 16) CPA_SC(64, 32) CPA_SC(64, 64) CPA_SC(64, 128)
+  CPA_SC(128, 16) CPA_SC(128, 32) CPA_SC(128, 64) CPA_SC(128, 128)
+#undef CPA_SC
+  return -1;
+}
+
+cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
+                          cudaStream_t st, int* launches) {
+  k_pool_q<<<dim3(g.nqb, g.Hq, g.B), g.d, 0, st>>>(q, g, qbar, mstar_key);
+  ++*launches;
+  if (g.Rpad > g.R) {
+    const long long total = (long long)g.B * g.Gn * (g.Rpad - g.R) * g.d;
+    const int blocks = (int)((total + 255) / 256 < 1024 ? (total + 255) / 256 : 1024);
+    k_pool_pad<<<blocks, 256, 0, st>>>(g, qbar);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+template <int D, int BS>
+static cudaError_t launch_scores_t(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
+                                   const Geo& g, float* scores, int* mstar_key, int num_sms,
+                                   cudaStream_t st) {
+  using Cfg = ScoreCfg<D, BS>;
+  auto kern = k_block_scores<D, BS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+  if (e != cudaSuccess) return e;
+  const int units = g.B * g.Gn * (g.Rpad / 128);
+  int splits = num_sms / units;
+  if (splits < 1) splits = 1;
+  if (splits > g.nkvb) splits = g.nkvb;
+  const int ppc = (g.nkvb + splits - 1) / splits;
+  splits = (g.nkvb + ppc - 1) / ppc;
+  kern<<<dim3(splits, g.Rpad / 128, g.B * g.Gn), 192, Cfg::kSmem, st>>>(tq, tk, pt, g, ppc, scores,
+                                                                         mstar_key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_scores(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
+                                const Geo& g, float* scores, int* mstar_key, int num_sms,
+                                cudaStream_t st, int* launches) {
+  ++*launches;
+#define CPA_SC(DD, BB) \
+  if (g.d == DD && g.bs == BB) return launch_scores_t<DD, BB>(tq, tk, pt, g, scores, mstar_key, num_sms, st);
+  CPA_SC(64, 16) CPA_SC(64, 32) CPA_SC(64, 64) CPA_SC(64, 128)
+  CPA_SC(128, 16) CPA_SC(128, 32) CPA_SC(128, 64) CPA_SC(128, 128)
+#undef CPA_SC
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace cpa

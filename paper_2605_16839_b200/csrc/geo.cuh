@@ -1,0 +1,24 @@
+// geo.cuh -- chunk geometry passed by value to every libcpa kernel.
+#pragma once
+#include <stdint.h>
+
+namespace cpa {
+
+struct Geo {
+  int B, Hq, Hkv, d, bs, E, Gn, C, P, L;
+  int nqb, nkvb, pb, nwords;
+  int R, Rpad;       // estimator rows per group: R = E*nqb, Rpad = 128*ceil(R/128)
+  int maxb;          // page_table row length
+  int kv_per_q;      // Hq/Hkv
+  float scale;       // softmax / score scale
+  float ln_alpha;
+  uint32_t flags;
+  long long q_stride;  // elements between tokens of q / o
+};
+
+// KV head of execution group g: its query heads [g*E, (g+1)*E) all read KV head (g*E)/(Hq/Hkv).
+__host__ __device__ inline int group_kv_head(const Geo& g, int grp) {
+  return (grp * g.E) / g.kv_per_q;
+}
+
+}  // namespace cpa
