@@ -10,8 +10,9 @@
 // share every K/V page (GQA packing), FA4-style ping-pong:
 //   warps 0-3  softmax for tile 0 (one TMEM lane = one query row per thread)
 //   warps 4-7  softmax for tile 1
-//   warp  8    TMA producer: kv_indices -> page_table -> cp.async.bulk.tensor K/V pages
-//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 8-9  V converter: each landed bf16 V tile -> fp16 in place (P.V runs in fp16, DESIGN K3)
+//   warp  10   TMA producer: kv_indices -> page_table -> cp.async.bulk.tensor K/V pages
+//   warp  11   TMEM allocator + single-thread tcgen05.mma issuer
 // TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+d) O1 [384,384+d); P_t (bf16) aliases S_t.
 // MMA order per KV block n: PV0(n), S0(n+1), PV1(n), S1(n+1) -- softmax of one tile overlaps the
 // tensor-core work of the other. Online softmax in the log2 domain with lazy rescaling of O
@@ -29,7 +30,8 @@ struct AttnCfg {
   static constexpr int kKStages = (BS * D >= 128 * 128) ? 3 : 4;
   static constexpr int kVStages = (BS * D >= 128 * 128) ? 2 : 4;
   static constexpr int kSoftmaxWarps = 4 * NT;
-  static constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
+  static constexpr int kConvWarps = 2;             // bf16 -> fp16 in-place conversion of V tiles
+  static constexpr int kThreads = (kSoftmaxWarps + kConvWarps + 2) * 32;
   static constexpr int kTmemCols = NT == 2 ? 512 : 256;
   static constexpr int kSCol0 = 0;                 // S_t at t*128
   static constexpr int kOCol0 = NT * 128;          // O_t at kOCol0 + t*128
@@ -61,7 +63,8 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   uint64_t* k_empty = k_full + Cfg::kKStages;
   uint64_t* v_full = k_empty + Cfg::kKStages;
   uint64_t* v_empty = v_full + Cfg::kVStages;
-  uint64_t* s_full = v_empty + Cfg::kVStages;   // [NT]
+  uint64_t* v_ready = v_empty + Cfg::kVStages;  // [kVStages] V tile converted to fp16
+  uint64_t* s_full = v_ready + Cfg::kVStages;   // [NT]
   uint64_t* p_full = s_full + NT;               // [NT]
   uint64_t* o_full = p_full + NT;               // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
@@ -83,7 +86,9 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   const int kvh = group_kv_head(g, grp);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  constexpr uint32_t kTmaWarp = Cfg::kSoftmaxWarps, kMmaWarp = Cfg::kSoftmaxWarps + 1;
+  constexpr uint32_t kConvWarp0 = Cfg::kSoftmaxWarps;
+  constexpr uint32_t kTmaWarp = kConvWarp0 + Cfg::kConvWarps, kMmaWarp = kTmaWarp + 1;
+  const bool p_bf16 = (g.flags & (1u << 8)) != 0;  // ablation: bf16 P with the bf16 V as stored
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch_desc(&tm_q);
@@ -91,7 +96,11 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     tma_prefetch_desc(&tm_v);
     mbar_init(q_full, 1);
     for (int s = 0; s < Cfg::kKStages; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
-    for (int s = 0; s < Cfg::kVStages; ++s) { mbar_init(v_full + s, 1); mbar_init(v_empty + s, 1); }
+    for (int s = 0; s < Cfg::kVStages; ++s) {
+      mbar_init(v_full + s, 1);
+      mbar_init(v_empty + s, 1);
+      mbar_init(v_ready + s, Cfg::kConvWarps);
+    }
     for (int t = 0; t < NT; ++t) { mbar_init(s_full + t, 1); mbar_init(p_full + t, 4); }
     mbar_init(o_full, 1);
     fence_barrier_init();
@@ -149,7 +158,8 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   } else if (warp == kMmaWarp) {
     if (lane == 0 && N > 0) {  // ------------------------------------------------ MMA issuer
       constexpr uint32_t idesc_s = umma_idesc_bf16(128, BS, 0, 0);
-      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, 0, 1);
+      // P (A, TMEM) and V (B, smem) are fp16 unless CPA_F_P_BF16: a/b formats [7,10)/[10,13) = 0 (f16)
+      const uint32_t idesc_o = umma_idesc_bf16(128, D, 0, 1) & ~(p_bf16 ? 0u : ((7u << 7) | (7u << 10)));
       const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
       auto issue_s = [&](int t, int ks) {
         const uint32_t d_tm = tmem + Cfg::kSCol0 + t * 128;
@@ -184,7 +194,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
         const int vs = n % Cfg::kVStages;
         const int ks1 = (n + 1) % Cfg::kKStages;
         const bool more = n + 1 < N;
-        mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
+        mbar_wait(v_ready + vs, (n / Cfg::kVStages) & 1);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           mbar_wait(p_full + t, n & 1);
@@ -203,6 +213,29 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
         if (more) tc_commit(k_empty + ks1);
       }
       tc_commit(o_full);
+    }
+  } else if (warp >= kConvWarp0) {  // --------------------------------------- V bf16 -> fp16
+    // P is rounded to fp16 (2^-11) instead of bf16 (2^-8); tcgen05 kind::f16 needs A and B of one
+    // type, so each landed V tile is converted in place (same swizzled layout: elementwise).
+    const int ct = (warp - kConvWarp0) * 32 + lane;
+    for (int n = 0; n < N; ++n) {
+      const int vs = n % Cfg::kVStages;
+      mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
+      if (!p_bf16) {
+        uint4* tile = reinterpret_cast<uint4*>(sV + vs * Cfg::kKVBytes);
+#pragma unroll 4
+        for (int x = ct; x < Cfg::kKVBytes / 16; x += Cfg::kConvWarps * 32) {
+          uint4 w = tile[x];
+          w.x = bf16x2_to_f16x2(w.x);
+          w.y = bf16x2_to_f16x2(w.y);
+          w.z = bf16x2_to_f16x2(w.z);
+          w.w = bf16x2_to_f16x2(w.w);
+          tile[x] = w;
+        }
+        fence_proxy_async_smem();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(v_ready + vs);
     }
   } else {  // ------------------------------------------------------------------ softmax / epilogue
     const int t = warp / 4;           // Q tile of this warpgroup
@@ -252,7 +285,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
         const float e0 = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -m_use));
         const float e1 = fast_exp2(fmaf(__uint_as_float(s[c + 1]), sl2, -m_use));
         lsum += e0 + e1;
-        pk[c / 2] = pack_bf16x2(e0, e1);
+        pk[c / 2] = p_bf16 ? pack_bf16x2(e0, e1) : pack_f16x2(e0, e1);
       }
       l_run = l_run * f + lsum;
       if constexpr (BS >= 32) {
@@ -261,7 +294,8 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
       } else {
         tmem_st8(s_tm, *reinterpret_cast<uint32_t(*)[8]>(pk));
       }
-      if (rescale && n > 0) {  // O_t += ... of block n-1 is complete (implied by s_full, see header)
+      // tcgen05.ld/st are warp-collective: rescale O when any row of the warp needs it (f = 1 else)
+      if (__any_sync(0xffffffffu, rescale && n > 0)) {  // PV_t(n-1) complete (implied by s_full)
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
           uint32_t o[32];
