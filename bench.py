@@ -164,11 +164,9 @@ def run_gpu(args):
     seed = seed_of(args.config)
     P, C, L = cfg.chunk_geometry()
     bs, d, E = cfg.block_size, cfg.head_dim, cfg.group_size
-    assert cfg.num_kv_heads % world == 0, "KV groups must divide over ranks"
-    hkv_l = cfg.num_kv_heads // world
-    kvh = range(rank * hkv_l, (rank + 1) * hkv_l)
-    qh = range(rank * hkv_l * E, (rank + 1) * hkv_l * E)
-    hq_l = len(qh)
+    from paper_2605_16839_b200.shard import allgather_heads, head_shard
+    kvh, qh = head_shard(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
+    hkv_l, hq_l = len(kvh), len(qh)
     k, v = make_kv(cfg, seed, RHO, kv_heads=kvh)
     q = make_q(cfg, seed, q_heads=qh)
     nkvb = -(-L // bs)
@@ -190,7 +188,7 @@ def run_gpu(args):
     def step():
         cpa.chunk_step(p, dq, cache, tables, o, kc, vc, workspace=ws)
         if world > 1:
-            dist.all_gather_into_tensor(o_all, o)
+            allgather_heads(o, o_all)
 
     def timed(fn, iters, warm):
         for _ in range(warm):
@@ -210,7 +208,7 @@ def run_gpu(args):
     # ---- headline: W warm-up steps, K timed steps, barrier + sync on both sides
     for _ in range(args.warmup):
         step()
-    launches_per_step = cpa.last_launch_count() if world == 1 else cpa.last_launch_count()
+    launches_per_step = cpa.last_launch_count()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -251,10 +249,7 @@ def run_gpu(args):
         vc2.copy_(hv_pin, non_blocking=True)
         cpa.chunk_step(p, dq2, cache, tables, o, kc2, vc2, workspace=ws)
         if world > 1:
-            dist.all_gather_into_tensor(o_all, o)
-            ho = o_all
-        else:
-            ho = o
+            allgather_heads(o, o_all)
         ho_pin.copy_(o, non_blocking=True)
 
     e2e_ms = float(np.mean(timed(e2e_step, args.steps, 1)))
