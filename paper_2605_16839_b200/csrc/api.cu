@@ -30,6 +30,9 @@ struct AttnArgs {
 };
 cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
+bool attn_2cta_supported(const Geo& g);
+cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
+                                        const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g,
                           long long page_stride, long long head_stride, cudaStream_t st, int* launches);
 cudaError_t launch_row_max(const int* mstar_key, const Geo& g, float* row_max, cudaStream_t st,
@@ -204,10 +207,10 @@ int q_map(CUtensorMap* m, const void* q, const Geo& g) {
   return make_map(m, q, 4, dims, str, box, "q");
 }
 int kv_map(CUtensorMap* m, const void* pages, const Geo& g, int num_pages, long long ps, long long hs,
-           const char* what) {
+           const char* what, int box_rows = 0) {
   cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.bs, (cuuint64_t)g.Hkv, (cuuint64_t)num_pages};
   cuuint64_t str[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)hs * 2, (cuuint64_t)ps * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)g.bs, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)(box_rows ? box_rows : g.bs), 1, 1};
   return make_map(m, pages, 4, dims, str, box, what);
 }
 
@@ -273,7 +276,14 @@ int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_k
   a.indices = t ? t->kv_indices : nullptr;
   a.out = o;
   a.out_f32 = (p->flags & CPA_F_OUT_F32) ? 1 : 0;
-  cudaError_t e = launch_paged_attention(tq, tk, tv, g, a, st, &g_launches);
+  cudaError_t e;
+  if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA)) {
+    CUtensorMap tkh;  // half a page of keys per CTA of the pair
+    if ((s = kv_map(&tkh, c->k_pages, g, c->num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
+    e = launch_paged_attention_2cta(tq, tkh, tv, g, a, st, &g_launches);
+  } else {
+    e = launch_paged_attention(tq, tk, tv, g, a, st, &g_launches);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "paged_attention");
   return CPA_OK;
 }

@@ -7,24 +7,36 @@
 //   O[b,p,h] = sum_{t in A(p)} softmax_t(scale q_p.k_t) v_t,  A(p) = {t : t/bs in T[b,h/E], t <= P+p}.
 //
 // CTA = (b, g, 128-token q-tile, pair of query heads of g) -> NT=2 Q tiles of 128 rows that
-// share every K/V page (GQA packing), FA4-style ping-pong:
+// share every K/V page (GQA packing). Warp roles:
 //   warps 0-3  softmax for tile 0 (one TMEM lane = one query row per thread)
 //   warps 4-7  softmax for tile 1
 //   warps 8-9  V converter: each landed bf16 V tile -> fp16 in place (P.V runs in fp16, DESIGN K3)
 //   warp  10   TMA producer: kv_indices -> page_table -> cp.async.bulk.tensor K/V pages
 //   warp  11   TMEM allocator + single-thread tcgen05.mma issuer
-// TMEM columns: S0 [0,128) S1 [128,256) O0 [256,256+d) O1 [384,384+d); P_t (bf16) aliases S_t.
-// MMA order per KV block n: PV0(n), S0(n+1), PV1(n), S1(n+1) -- softmax of one tile overlaps the
-// tensor-core work of the other. Online softmax in the log2 domain with lazy rescaling of O
-// (only when the running max grows by > 8, i.e. P <= 256, fp32 accumulators).
+// Each page is processed as SPB sub-blocks of SB = min(bs, 64) keys. TMEM (512 columns):
+//   S_t^0 [t*128, +64)  S_t^1 [t*128+64, +64)  O_t [NT*128 + t*128, +d)      (P_t aliases S_t^b)
+// S is double-buffered per tile, so the tensor core computes S_t(u+1) while the softmax of
+// S_t(u) runs; the softmax is the only serial link (S_t(u) -> P_t(u) -> PV_t(u)).
+// MMA order per sub-block u: PV_0(u), S_0(u+2), PV_1(u), S_1(u+2). Online softmax in the log2
+// domain with lazy O rescaling (only when the running max grows by > 8, so P <= 256).
 #include "common.cuh"
 #include "geo.cuh"
 
 namespace cpa {
 
+#ifdef CPA_TRACE
+__device__ long long g_trace[16][2048];
+#define TRACE(e, i) \
+  do { if (blockIdx.x == 0 && (i) < 2048) g_trace[e][i] = clock64(); } while (0)
+#else
+#define TRACE(e, i) do {} while (0)
+#endif
+
 template <int D, int BS, int NT>
 struct AttnCfg {
   static constexpr int kAtoms = D / 64;
+  static constexpr int SB = BS < 64 ? BS : 64;      // keys per sub-block (one S MMA, one softmax step)
+  static constexpr int SPB = BS / SB;               // sub-blocks per page
   static constexpr int kQBytes = 128 * D * 2;
   static constexpr int kKVBytes = BS * D * 2;
   static constexpr int kKStages = (BS * D >= 128 * 128) ? 3 : 4;
@@ -33,8 +45,7 @@ struct AttnCfg {
   static constexpr int kConvWarps = 2;             // bf16 -> fp16 in-place conversion of V tiles
   static constexpr int kThreads = (kSoftmaxWarps + kConvWarps + 2) * 32;
   static constexpr int kTmemCols = NT == 2 ? 512 : 256;
-  static constexpr int kSCol0 = 0;                 // S_t at t*128
-  static constexpr int kOCol0 = NT * 128;          // O_t at kOCol0 + t*128
+  static constexpr int kOCol0 = NT * 128;          // O_t at kOCol0 + t*128; S_t^b at t*128 + b*64
   static constexpr int kSmem = NT * kQBytes + (kKStages + kVStages) * kKVBytes + 1024 + 512;
   static_assert(kSmem <= 232448, "shared memory budget");
 };
@@ -47,11 +58,12 @@ struct AttnArgs {
   int out_f32;
 };
 
-template <int D, int BS, int NT>
+template <int D, int BS, int NT, bool PF16>
 __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     k_paged_attn(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                  const __grid_constant__ CUtensorMap tm_v, Geo g, AttnArgs args) {
   using Cfg = AttnCfg<D, BS, NT>;
+  constexpr int SB = Cfg::SB, SPB = Cfg::SPB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -64,9 +76,10 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   uint64_t* v_full = k_empty + Cfg::kKStages;
   uint64_t* v_empty = v_full + Cfg::kVStages;
   uint64_t* v_ready = v_empty + Cfg::kVStages;  // [kVStages] V tile converted to fp16
-  uint64_t* s_full = v_ready + Cfg::kVStages;   // [NT]
-  uint64_t* p_full = s_full + NT;               // [NT]
-  uint64_t* o_full = p_full + NT;               // [1]
+  uint64_t* s_full = v_ready + Cfg::kVStages;   // [NT][2]
+  uint64_t* p_full = s_full + 2 * NT;           // [NT][2] (per S buffer: the softmax may run 2 ahead)
+  uint64_t* pv_done = p_full + 2 * NT;          // [NT]
+  uint64_t* o_full = pv_done + NT;              // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
   int* n_blocks_s = reinterpret_cast<int*>(tmem_slot + 1);
   int* row_start_s = n_blocks_s + 1;
@@ -88,7 +101,6 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   constexpr uint32_t kConvWarp0 = Cfg::kSoftmaxWarps;
   constexpr uint32_t kTmaWarp = kConvWarp0 + Cfg::kConvWarps, kMmaWarp = kTmaWarp + 1;
-  const bool p_bf16 = (g.flags & (1u << 8)) != 0;  // ablation: bf16 P with the bf16 V as stored
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch_desc(&tm_q);
@@ -101,7 +113,13 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
       mbar_init(v_empty + s, 1);
       mbar_init(v_ready + s, Cfg::kConvWarps);
     }
-    for (int t = 0; t < NT; ++t) { mbar_init(s_full + t, 1); mbar_init(p_full + t, 4); }
+    for (int t = 0; t < NT; ++t) {
+      mbar_init(s_full + 2 * t, 1);
+      mbar_init(s_full + 2 * t + 1, 1);
+      mbar_init(p_full + 2 * t, 4);
+      mbar_init(p_full + 2 * t + 1, 4);
+      mbar_init(pv_done + t, 1);
+    }
     mbar_init(o_full, 1);
     fence_barrier_init();
     // number of table entries this q-tile can see: ascending j with j*bs <= P + last query
@@ -127,92 +145,131 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int N = *n_blocks_s;
+  const int N = *n_blocks_s;          // pages
+  const int U = N * SPB;              // sub-blocks
   const int row_start = *row_start_s;
 
+  // TMA and MMA roles run on all 32 lanes with warp-uniform control flow (so descriptors and
+  // coordinates live in uniform registers); one elected lane issues each TMA / tcgen05 instruction.
   if (warp == kTmaWarp) {
-    if (lane == 0 && N > 0) {  // ------------------------------------------------ TMA producer
-      mbar_expect_tx(q_full, NT * Cfg::kQBytes);
+    if (N > 0) {  // ------------------------------------------------------------ TMA producer
+      if (elect_one()) {
+        mbar_expect_tx(q_full, NT * Cfg::kQBytes);
 #pragma unroll
-      for (int t = 0; t < NT; ++t)
+        for (int t = 0; t < NT; ++t)
 #pragma unroll
-        for (int a = 0; a < Cfg::kAtoms; ++a)
-          tma_load_4d(sQ + t * Cfg::kQBytes + a * 128 * 128, &tm_q, q_full, 64 * a, h0 + t, p0, b);
+          for (int a = 0; a < Cfg::kAtoms; ++a)
+            tma_load_4d(sQ + t * Cfg::kQBytes + a * 128 * 128, &tm_q, q_full, 64 * a, h0 + t, p0, b);
+      }
+      __syncwarp();
       const int32_t* ptab = args.page_table + (long long)b * g.maxb;
       for (int n = 0; n < N; ++n) {
         const int j = args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
         const int page = __ldg(ptab + j);
         const int ks = n % Cfg::kKStages, vs = n % Cfg::kVStages;
         mbar_wait(k_empty + ks, ((n / Cfg::kKStages) & 1) ^ 1);
-        mbar_expect_tx(k_full + ks, Cfg::kKVBytes);
+        if (elect_one()) {
+          mbar_expect_tx(k_full + ks, Cfg::kKVBytes);
 #pragma unroll
-        for (int a = 0; a < Cfg::kAtoms; ++a)
-          tma_load_4d(sK + ks * Cfg::kKVBytes + a * BS * 128, &tm_k, k_full + ks, 64 * a, 0, kvh, page);
+          for (int a = 0; a < Cfg::kAtoms; ++a)
+            tma_load_4d(sK + ks * Cfg::kKVBytes + a * BS * 128, &tm_k, k_full + ks, 64 * a, 0, kvh, page);
+        }
+        __syncwarp();
         mbar_wait(v_empty + vs, ((n / Cfg::kVStages) & 1) ^ 1);
-        mbar_expect_tx(v_full + vs, Cfg::kKVBytes);
+        if (elect_one()) {
+          mbar_expect_tx(v_full + vs, Cfg::kKVBytes);
 #pragma unroll
-        for (int a = 0; a < Cfg::kAtoms; ++a)
-          tma_load_4d(sV + vs * Cfg::kKVBytes + a * BS * 128, &tm_v, v_full + vs, 64 * a, 0, kvh, page);
+          for (int a = 0; a < Cfg::kAtoms; ++a)
+            tma_load_4d(sV + vs * Cfg::kKVBytes + a * BS * 128, &tm_v, v_full + vs, 64 * a, 0, kvh, page);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0 && N > 0) {  // ------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc_s = umma_idesc_bf16(128, BS, 0, 0);
+    if (N > 0) {  // ------------------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc_s = umma_idesc_bf16(128, SB, 0, 0);
       // P (A, TMEM) and V (B, smem) are fp16 unless CPA_F_P_BF16: a/b formats [7,10)/[10,13) = 0 (f16)
-      const uint32_t idesc_o = umma_idesc_bf16(128, D, 0, 1) & ~(p_bf16 ? 0u : ((7u << 7) | (7u << 10)));
+      constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, 0, 1) & ~(PF16 ? ((7u << 7) | (7u << 10)) : 0u);
       const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
-      auto issue_s = [&](int t, int ks) {
-        const uint32_t d_tm = tmem + Cfg::kSCol0 + t * 128;
+      // S_t(u) = Q_t K_(u)^T over SB keys into S_t^{u%2}; commit -> s_full[t][u%2]
+      auto issue_s = [&](int t, int u) {
+        const int n = u / SPB, h = u % SPB;
+        const uint32_t d_tm = tmem + t * 128 + (u & 1) * 64;
+        const uint32_t kb = k_base + (n % Cfg::kKStages) * Cfg::kKVBytes + h * SB * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int a = 0; a < Cfg::kAtoms; ++a)
+          for (int a = 0; a < Cfg::kAtoms; ++a)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = umma_desc_sw128(q_base + t * Cfg::kQBytes + a * 128 * 128 + kk * 32, 16, 1024);
-            const uint64_t bd = umma_desc_sw128(k_base + ks * Cfg::kKVBytes + a * BS * 128 + kk * 32, 16, 1024);
-            mma_ss(d_tm, ad, bd, idesc_s, (a | kk) != 0);
-          }
-      };
-      auto issue_pv = [&](int t, int vs, int n) {
-        const uint32_t d_tm = tmem + Cfg::kOCol0 + t * 128;
-        const uint32_t p_tm = tmem + Cfg::kSCol0 + t * 128;
-#pragma unroll
-        for (int kk = 0; kk < BS / 16; ++kk) {
-          const uint64_t bd = umma_desc_sw128(v_base + vs * Cfg::kKVBytes + kk * 16 * 128, BS * 128, 1024);
-          mma_ts(d_tm, p_tm + kk * 8, bd, idesc_o, (n > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t ad = umma_desc_sw128(q_base + t * Cfg::kQBytes + a * 128 * 128 + kk * 32, 16, 1024);
+              const uint64_t bd = umma_desc_sw128(kb + a * BS * 128 + kk * 32, 16, 1024);
+              mma_ss(d_tm, ad, bd, idesc_s, (a | kk) != 0);
+            }
+          tc_commit(s_full + 2 * t + (u & 1));
         }
+        __syncwarp();
+      };
+      // O_t += P_t(u) V_(u): A = P in TMEM (fp16 pairs over S_t^{u%2}), B = V rows of the sub-block
+      auto issue_pv = [&](int t, int u) {
+        const int n = u / SPB, h = u % SPB;
+        const uint32_t d_tm = tmem + Cfg::kOCol0 + t * 128;
+        const uint32_t p_tm = tmem + t * 128 + (u & 1) * 64;
+        const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kKVBytes + h * SB * 128;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < SB / 16; ++kk) {
+            const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
+            mma_ts(d_tm, p_tm + kk * 8, bd, idesc_o, (u > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(pv_done + t);
+        }
+        __syncwarp();
+      };
+      auto commit1 = [&](uint64_t* bar) {
+        if (elect_one()) tc_commit(bar);
+        __syncwarp();
+      };
+      auto wait_k = [&](int u) {  // first sub-block of a page: its K must have landed
+        if (u % SPB == 0) {
+          const int n = u / SPB;
+          mbar_wait(k_full + n % Cfg::kKStages, (n / Cfg::kKStages) & 1);
+          tc_fence_after();
+        }
+      };
+      auto release_k = [&](int u) {  // after the last S of a page (both tiles) was issued
+        if (u % SPB == SPB - 1) commit1(k_empty + (u / SPB) % Cfg::kKStages);
       };
       mbar_wait(q_full, 0);
-      mbar_wait(k_full + 0, 0);
       tc_fence_after();
+      for (int u = 0; u < 2 && u < U; ++u) {
+        wait_k(u);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        issue_s(t, 0);
-        tc_commit(s_full + t);
+        for (int t = 0; t < NT; ++t) issue_s(t, u);
+        release_k(u);
       }
-      tc_commit(k_empty + 0);
-      for (int n = 0; n < N; ++n) {
-        const int vs = n % Cfg::kVStages;
-        const int ks1 = (n + 1) % Cfg::kKStages;
-        const bool more = n + 1 < N;
-        mbar_wait(v_ready + vs, (n / Cfg::kVStages) & 1);
+      for (int u = 0; u < U; ++u) {
+        const int n = u / SPB;
+        if (u % SPB == 0) {
+          mbar_wait(v_ready + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
+          if (lane == 0) TRACE(1, n);
+        }
+        const bool more = u + 2 < U;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          mbar_wait(p_full + t, n & 1);
+          mbar_wait(p_full + 2 * t + (u & 1), (u >> 1) & 1);
+          if (lane == 0) TRACE(2, 2 * u + t);
           tc_fence_after();
-          issue_pv(t, vs, n);
+          issue_pv(t, u);
           if (more) {
-            if (t == 0) {
-              mbar_wait(k_full + ks1, ((n + 1) / Cfg::kKStages) & 1);
-              tc_fence_after();
-            }
-            issue_s(t, ks1);
-            tc_commit(s_full + t);
+            if (t == 0) wait_k(u + 2);
+            issue_s(t, u + 2);
           }
+          if (lane == 0) TRACE(3, 2 * u + t);
         }
-        tc_commit(v_empty + vs);
-        if (more) tc_commit(k_empty + ks1);
+        if (u % SPB == SPB - 1) commit1(v_empty + n % Cfg::kVStages);
+        if (more) release_k(u + 2);
       }
-      tc_commit(o_full);
+      commit1(o_full);
     }
   } else if (warp >= kConvWarp0) {  // --------------------------------------- V bf16 -> fp16
     // P is rounded to fp16 (2^-11) instead of bf16 (2^-8); tcgen05 kind::f16 needs A and B of one
@@ -221,7 +278,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     for (int n = 0; n < N; ++n) {
       const int vs = n % Cfg::kVStages;
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
-      if (!p_bf16) {
+      if constexpr (PF16) {
         uint4* tile = reinterpret_cast<uint4*>(sV + vs * Cfg::kKVBytes);
 #pragma unroll 4
         for (int x = ct; x < Cfg::kKVBytes / 16; x += Cfg::kConvWarps * 32) {
@@ -246,56 +303,81 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     const int lim = min(g.P + p, g.L - 1);  // last visible absolute key
     const float sl2 = g.scale * 1.4426950408889634f;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t s_tm = tmem + lane_off + Cfg::kSCol0 + t * 128;
     const uint32_t o_tm = tmem + lane_off + Cfg::kOCol0 + t * 128;
+    constexpr int CH = SB >= 32 ? 32 : SB;
+    constexpr int NCH = SB / CH;
     float m_run = -INFINITY, l_run = 0.f;
-    for (int n = 0; n < N; ++n) {
-      const int j = args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
-      mbar_wait(s_full + t, n & 1);
+    int j = 0;
+    for (int u = 0; u < U; ++u) {
+      if (u % SPB == 0) j = args.indptr != nullptr ? __ldg(args.indices + row_start + u / SPB) : u / SPB;
+      const uint32_t s_tm = tmem + lane_off + t * 128 + (u & 1) * 64;
+      if (row == 0) TRACE(4, 2 * u + t);
+      mbar_wait(s_full + 2 * t + (u & 1), (u >> 1) & 1);
+      if (row == 0) TRACE(5, 2 * u + t);
       tc_fence_after();
-      uint32_t s[BS];
-      if constexpr (BS >= 32) {
+      uint32_t sv[NCH][CH];
 #pragma unroll
-        for (int c0 = 0; c0 < BS; c0 += 32) tmem_ld32(s_tm + c0, *reinterpret_cast<uint32_t(*)[32]>(s + c0));
-      } else {
-        tmem_ld16(s_tm, *reinterpret_cast<uint32_t(*)[16]>(s));
+      for (int k = 0; k < NCH; ++k) {
+        if constexpr (CH == 32) tmem_ld32(s_tm + k * CH, sv[k]);
+        else tmem_ld16(s_tm + k * CH, sv[k]);
       }
       tmem_wait_ld();
-      const int tbase = j * g.bs;
-      if (tbase + BS - 1 > g.P + p0) {  // block crosses the causal diagonal of this tile
+      const int tbase = j * g.bs + (u % SPB) * SB;
+      if (tbase + SB - 1 > g.P + p0) {  // sub-block crosses the causal diagonal of this tile
 #pragma unroll
-        for (int c = 0; c < BS; ++c)
-          if (tbase + c > lim) s[c] = __float_as_uint(-INFINITY);
+        for (int k = 0; k < NCH; ++k)
+#pragma unroll
+          for (int c = 0; c < CH; ++c)
+            if (tbase + k * CH + c > lim) sv[k][c] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < BS; ++c) mx = fmaxf(mx, __uint_as_float(s[c]));
-      const float m_blk = mx * sl2;
+      for (int k = 0; k < NCH; ++k)
+#pragma unroll
+        for (int c = 0; c < CH; c += 8)
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4)
+            m4[w4] = fmax3(m4[w4], __uint_as_float(sv[k][c + 2 * w4]), __uint_as_float(sv[k][c + 2 * w4 + 1]));
+      const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
       float f = 1.f;
-      const bool rescale = m_blk > m_run + 8.0f;  // lazy rescale (first block always lands here)
+      const bool rescale = m_blk > m_run + 8.0f;  // lazy rescale (first sub-block always lands here)
       if (rescale) {
-        if (n > 0) f = fast_exp2(m_run - m_blk);
+        if (u > 0) f = fast_exp2(m_run - m_blk);
         m_run = m_blk;
       }
       const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      float lsum = 0.f;
-      uint32_t pk[BS / 2];
+      if (row == 0) TRACE(11, 2 * u + t);
+      // P = exp2(s*sl2 - m): packed f32x2 FFMA; pairs selected by use_poly_exp go through a degree-3
+      // polynomial on the FMA pipe (MUFU offload), the rest through MUFU.EX2; 4 independent f32x2
+      // partial sums; each chunk is packed (fp16) and stored over S in TMEM.
+      float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
-      for (int c = 0; c < BS; c += 2) {
-        const float e0 = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -m_use));
-        const float e1 = fast_exp2(fmaf(__uint_as_float(s[c + 1]), sl2, -m_use));
-        lsum += e0 + e1;
-        pk[c / 2] = p_bf16 ? pack_bf16x2(e0, e1) : pack_f16x2(e0, e1);
-      }
-      l_run = l_run * f + lsum;
-      if constexpr (BS >= 32) {
+      for (int k = 0; k < NCH; ++k) {
+        uint32_t pk[CH / 2];
 #pragma unroll
-        for (int c0 = 0; c0 < BS / 2; c0 += 16) tmem_st16(s_tm + c0, *reinterpret_cast<uint32_t(*)[16]>(pk + c0));
-      } else {
-        tmem_st8(s_tm, *reinterpret_cast<uint32_t(*)[8]>(pk));
+        for (int q2 = 0; q2 < CH / 2; ++q2) {
+          float2 x = ffma2(make_float2(__uint_as_float(sv[k][2 * q2]), __uint_as_float(sv[k][2 * q2 + 1])), sl2, -m_use);
+          float2 e;
+          if (PF16 && use_poly_exp(q2)) {
+            e = exp2_poly2(x);
+          } else {
+            e.x = fast_exp2(x.x);
+            e.y = fast_exp2(x.y);
+          }
+          acc[q2 & 3] = fadd2(acc[q2 & 3], e);
+          pk[q2] = PF16 ? pack_f16x2(e.x, e.y) : pack_bf16x2(e.x, e.y);
+        }
+        if constexpr (CH == 32) tmem_st16(s_tm + k * CH / 2, *reinterpret_cast<uint32_t(*)[16]>(pk));
+        else tmem_st8(s_tm + k * CH / 2, *reinterpret_cast<uint32_t(*)[8]>(pk));
       }
-      // tcgen05.ld/st are warp-collective: rescale O when any row of the warp needs it (f = 1 else)
-      if (__any_sync(0xffffffffu, rescale && n > 0)) {  // PV_t(n-1) complete (implied by s_full)
+      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+      l_run = l_run * f + ((a01.x + a01.y) + (a23.x + a23.y));
+      if (row == 0) TRACE(12, 2 * u + t);
+      // tcgen05.ld/st are warp-collective: rescale O when any row of the warp needs it (f = 1 else),
+      // after PV_t(u-1) has completed and before PV_t(u) is issued (it waits on p_full below).
+      if (__any_sync(0xffffffffu, rescale && u > 0)) {
+        mbar_wait(pv_done + t, (u - 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
           uint32_t o[32];
@@ -310,12 +392,13 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full + t);
+      if (lane == 0) mbar_arrive(p_full + 2 * t + (u & 1));
+      if (row == 0) TRACE(6, 2 * u + t);
     }
     // ---- epilogue: O = O_acc / l
     const bool store = p < g.C;
-    const float inv_l = (N > 0 && l_run > 0.f) ? 1.0f / l_run : 0.f;
-    if (N > 0) {
+    const float inv_l = (U > 0 && l_run > 0.f) ? 1.0f / l_run : 0.f;
+    if (U > 0) {
       mbar_wait(o_full, 0);
       tc_fence_after();
     }
@@ -323,7 +406,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t o[32];
-      if (N > 0) {
+      if (U > 0) {
         tmem_ld32(o_tm + c0, o);
         tmem_wait_ld();
       } else {
@@ -358,11 +441,11 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
 }
 
 // ---------------------------------------------------------------- launcher
-template <int D, int BS, int NT>
+template <int D, int BS, int NT, bool PF16>
 static cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                  const Geo& g, const AttnArgs& a, cudaStream_t st) {
   using Cfg = AttnCfg<D, BS, NT>;
-  auto kern = k_paged_attn<D, BS, NT>;
+  auto kern = k_paged_attn<D, BS, NT, PF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
   if (e != cudaSuccess) return e;
   const int nqt = (g.C + 127) / 128;
@@ -377,8 +460,11 @@ cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk,
   const bool pair = (g.E % 2) == 0;
 #define CPA_AT(DD, BB)                                                        \
   if (g.d == DD && g.bs == BB) {                                              \
-    return pair ? launch_attn_t<DD, BB, 2>(tq, tk, tv, g, a, st)              \
-                : launch_attn_t<DD, BB, 1>(tq, tk, tv, g, a, st);             \
+    if (g.flags & (1u << 8))                                                  \
+      return pair ? launch_attn_t<DD, BB, 2, false>(tq, tk, tv, g, a, st)     \
+                  : launch_attn_t<DD, BB, 1, false>(tq, tk, tv, g, a, st);    \
+    return pair ? launch_attn_t<DD, BB, 2, true>(tq, tk, tv, g, a, st)        \
+                : launch_attn_t<DD, BB, 1, true>(tq, tk, tv, g, a, st);       \
   }
   CPA_AT(64, 16) CPA_AT(64, 32) CPA_AT(64, 64) CPA_AT(64, 128)
   CPA_AT(128, 16) CPA_AT(128, 32) CPA_AT(128, 64) CPA_AT(128, 128)
@@ -387,3 +473,9 @@ cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk,
 }
 
 }  // namespace cpa
+
+#ifdef CPA_TRACE
+extern "C" __attribute__((visibility("default"))) int cpa_debug_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, cpa::g_trace, sizeof(cpa::g_trace));
+}
+#endif

@@ -16,6 +16,12 @@ CPA_DEV uint32_t smem_u32(const void* p) {
 }
 
 CPA_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
+// true on exactly one (the lowest) active lane of a converged warp
+CPA_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
 CPA_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 
 // ---------------------------------------------------------------- mbarrier
@@ -163,6 +169,67 @@ CPA_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
       : "memory");
 }
 
+// ---------------------------------------------------------------- 2-CTA (cluster pair) helpers
+CPA_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+CPA_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA 0 of the pair (peer bit cleared)
+CPA_DEV uint32_t leader_addr(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
+// arrive on the barrier at the same offset in CTA `cta` of the cluster
+CPA_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+// TMA load into this CTA's smem whose transaction bytes complete on the leader CTA's barrier
+CPA_DEV void tma_load_4d_2sm(void* smem_dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_addr(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+template <uint32_t NCOLS>
+CPA_DEV void tmem_alloc2(uint32_t* smem_slot) {  // whole warp, same warp id in both CTAs
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_slot)),
+               "n"(NCOLS)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t NCOLS>
+CPA_DEV void tmem_dealloc2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS) : "memory");
+}
+// commit all prior 2-CTA MMAs of this thread to the barrier at the same offset in both CTAs
+CPA_DEV void tc_commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+CPA_DEV void mma2_ss(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+CPA_DEV void mma2_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- UMMA descriptors
 // Shared-memory matrix descriptor (sm_100 "version 1"): start>>4 [0,14), LBO>>4 [16,30),
 // SBO>>4 [32,46), version=1 [46,48), base_offset=0 [49,52), lbo_mode=0 [52], layout [61,64).
@@ -203,6 +270,63 @@ CPA_DEV float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+CPA_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+CPA_DEV unsigned long long f2_as_u64(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+CPA_DEV float2 u64_as_f2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+// packed f32x2 (sm_100 FFMA2 / FADD2): a*s + c with scalar s, c broadcast
+CPA_DEV float2 ffma2(float2 a, float s, float c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(make_float2(s, s))),
+      "l"(f2_as_u64(make_float2(c, c))));
+  return u64_as_f2(r);
+}
+CPA_DEV float2 ffma2v(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)), "l"(f2_as_u64(c)));
+  return u64_as_f2(r);
+}
+CPA_DEV float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_as_u64(a)), "l"(f2_as_u64(b)));
+  return u64_as_f2(r);
+}
+// 2^x for a pair on the FMA pipe: x = j + f, j = rint(x), f in [-1/2, 1/2]; 2^f by a degree-3
+// minimax polynomial (max rel. error 7.5e-5 < fp16 half-ulp 2.4e-4); 2^j added to the exponent
+// field. x is clamped to >= -126 so the exponent never wraps (2^-126 ~ 0 in the softmax).
+CPA_DEV float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float kMagic = 12582912.f;  // 1.5 * 2^23: adding it rounds to an integer in the low bits
+  const float2 t = fadd2(x, make_float2(kMagic, kMagic));
+  const float2 r = fadd2(t, make_float2(-kMagic, -kMagic));
+  const float2 fr = fadd2(x, make_float2(-r.x, -r.y));
+  float2 p = ffma2v(fr, make_float2(0.05517605698815439f, 0.05517605698815439f),
+                    make_float2(0.24261150978022342f, 0.24261150978022342f));
+  p = ffma2v(p, fr, make_float2(0.6932601800069688f, 0.6932601800069688f));
+  p = ffma2v(p, fr, make_float2(0.9999280269517422f, 0.9999280269517422f));
+  float2 e;
+  e.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23));
+  e.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23));
+  return e;
+}
+// which pairs of a 32-column chunk take the polynomial path (6 of 16 = 3/8)
+#ifndef CPA_POLY_MASK
+#define CPA_POLY_MASK 0x12  // pairs 1 and 4 of every 8 (1/4 of the exps) use the polynomial
+#endif
+CPA_DEV constexpr bool use_poly_exp(int q2) { return ((CPA_POLY_MASK >> (q2 & 7)) & 1) != 0; }
+
 // Order-preserving float <-> int key for atomicMax on floats (incl. -inf).
 CPA_DEV int float_key(float f) {
   int i = __float_as_int(f);

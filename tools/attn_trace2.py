@@ -1,0 +1,34 @@
+"""Per-block event trace of cluster 0 (leader CTA) of k_paged_attn_2cta (build with -DCPA_TRACE)."""
+import os, sys, ctypes, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+os.environ["CPA_LIB_PATH"] = sys.argv[1]
+import paper_2605_16839_b200 as cpa
+from synth.workload import CONFIGS, make_kv, make_q, page_layout, to_pool
+cfg = CONFIGS[os.environ.get("CFG", "llama8b_32k")]
+seed = 16839 + list(CONFIGS).index(cfg.name)
+P, C, L = cfg.chunk_geometry(); bs = cfg.block_size
+k, v = make_kv(cfg, seed); q = make_q(cfg, seed)
+pt, npg = page_layout(cfg.batch, -(-L // bs), seed)
+dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
+cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)), torch.from_numpy(pt).cuda())
+dq = dev(q)
+p = cpa.make_params(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06)
+o = torch.empty(cfg.batch, C, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
+t = cpa.alloc_tables(p); cpa.build_tables(p, dq, cache, t)
+for _ in range(3): cpa.paged_attention(p, dq, cache, t, o)
+torch.cuda.synchronize()
+buf = (ctypes.c_longlong * (32 * 2048))()
+cpa.lib().cpa_debug_trace2(buf)
+tr = np.frombuffer(buf, dtype=np.int64).reshape(32, 2048)
+N = int((tr[2] > 0).sum())
+d = lambda a, b: int(a - b)
+per = [d(tr[2, n + 1], tr[2, n]) for n in range(2, N - 2)]
+print("blocks", N, "median period per 128-key page (cycles)", int(np.median(per)))
+for n in list(range(0, 4)) + list(range(N // 2, N // 2 + 4)):
+    print(json.dumps({"n": n, "period": d(tr[2, n + 1], tr[2, n]) if n + 1 < N else 0,
+        "mma_vready_wait": d(tr[1, n], tr[3, n - 1]) if n > 0 else 0, "mma_p_wait": d(tr[2, n], tr[1, n]),
+        "mma_pv_issue": d(tr[9, n], tr[2, n]), "mma_k_wait": d(tr[10, n], tr[9, n]), "mma_s_issue": d(tr[3, n], tr[10, n]),
+        "wg": n % 2, "sm_wait": d(tr[5 + 16*(n%2), n], tr[4 + 16*(n%2), n]),
+        "sm_ld_max": d(tr[11 + 16*(n%2), n], tr[5 + 16*(n%2), n]), "sm_exp": d(tr[12 + 16*(n%2), n], tr[11 + 16*(n%2), n]),
+        "sm_tail": d(tr[6 + 16*(n%2), n], tr[12 + 16*(n%2), n]), "conv": d(tr[8, n], tr[7, n])}))
