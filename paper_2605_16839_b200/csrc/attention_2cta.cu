@@ -252,7 +252,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const int vs = n % Cfg::kVStages;
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
       if (ct == 0) TRACE2(7, n);
+#ifndef CPA_EXP_NO_CONV
       if constexpr (PF16) {
+#else
+      if constexpr (false) {
+#endif
         // all loads first (16 x 16 B in flight per thread), then convert + store
         constexpr int kPer = Cfg::kVHalf / 16 / (Cfg::kConvWarps * 32);
         uint4* tile = reinterpret_cast<uint4*>(sV + vs * Cfg::kVHalf);
