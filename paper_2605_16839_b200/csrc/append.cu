@@ -6,25 +6,34 @@
 
 namespace cpa {
 
-// grid (C, Hkv, B), block d/8 threads: one 16-byte vector per thread for K and for V.
-__global__ void k_append(const uint4* __restrict__ kc, const uint4* __restrict__ vc, uint4* __restrict__ kp,
-                         uint4* __restrict__ vp, const int32_t* __restrict__ pt, Geo g, long long ps,
-                         long long hs) {
-  const int c = blockIdx.x, h = blockIdx.y, b = blockIdx.z, e = threadIdx.x;  // e: 8-element vector
-  const int t = g.P + c, j = t / g.bs, slot = t % g.bs;
-  const int page = __ldg(pt + (long long)b * g.maxb + j);
-  const long long src = (((long long)b * g.C + c) * g.Hkv + h) * (g.d / 8) + e;
-  const long long dst = ((long long)page * ps + (long long)h * hs + (long long)slot * g.d) / 8 + e;
-  kp[dst] = kc[src];
-  vp[dst] = vc[src];
+// flat grid-stride copy, one 16-byte vector per thread step: source [B, C, Hkv, d] is read
+// contiguously; each (token, head) row of d elements lands contiguous in its page slot.
+__global__ void __launch_bounds__(256) k_append(const uint4* __restrict__ kc, const uint4* __restrict__ vc,
+                                                uint4* __restrict__ kp, uint4* __restrict__ vp,
+                                                const int32_t* __restrict__ pt, Geo g, long long ps, long long hs) {
+  const int per_tok = g.Hkv * (g.d / 8);
+  const long long total = (long long)g.B * g.C * per_tok;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total; x += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(x % (g.d / 8));
+    const long long r = x / (g.d / 8);
+    const int h = (int)(r % g.Hkv);
+    const long long bc = r / g.Hkv;
+    const int c = (int)(bc % g.C), b = (int)(bc / g.C);
+    const int t = g.P + c, j = t / g.bs, slot = t % g.bs;
+    const int page = __ldg(pt + (long long)b * g.maxb + j);
+    const long long dst = ((long long)page * ps + (long long)h * hs + (long long)slot * g.d) / 8 + e;
+    kp[dst] = kc[x];
+    vp[dst] = vc[x];
+  }
 }
 
 cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g, long long ps,
                           long long hs, cudaStream_t st, int* launches) {
-  k_append<<<dim3(g.C, g.Hkv, g.B), g.d / 8, 0, st>>>(
-      reinterpret_cast<const uint4*>(kc), reinterpret_cast<const uint4*>(vc),
-      reinterpret_cast<uint4*>(c.k_pages), reinterpret_cast<uint4*>(c.v_pages),
-      c.page_table, g, ps, hs);
+  const long long total = (long long)g.B * g.C * g.Hkv * (g.d / 8);
+  const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+  k_append<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(kc), reinterpret_cast<const uint4*>(vc),
+                                   reinterpret_cast<uint4*>(c.k_pages), reinterpret_cast<uint4*>(c.v_pages),
+                                   c.page_table, g, ps, hs);
   ++*launches;
   return cudaGetLastError();
 }

@@ -13,22 +13,64 @@
 namespace cpa {
 
 // ---------------------------------------------------------------- a1: pool Q
-// grid (nqb, Hq, B), block d threads. qbar: [2][B*Gn*Rpad][d] bf16 (hi rows, then lo rows).
-__global__ void k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
-                         __nv_bfloat16* __restrict__ qbar, int* __restrict__ mstar_key) {
-  const int i = blockIdx.x, h = blockIdx.y, b = blockIdx.z, e = threadIdx.x;
+// grid (nqb, B, Hq*d/512), block 256 threads = 4 token quarters x 64 slab threads; a slab thread
+// owns 8 consecutive elements (one uint4) of a 512-element slice of [Hq*d]; each quarter sums a
+// quarter of the q-block's tokens (8 loads in flight), the quarters are combined in shared memory.
+// qbar: [2][B*Gn*Rpad][d] bf16 (hi rows, then lo rows).
+__global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
+                                                __nv_bfloat16* __restrict__ qbar, int* __restrict__ mstar_key) {
+  __shared__ float part[3][64][9];
+  const int i = blockIdx.x, b = blockIdx.y;
+  const int st = threadIdx.x & 63, quarter = threadIdx.x >> 6;
+  const int x0 = (blockIdx.z * 64 + st) * 8;  // element offset in [0, Hq*d)
   const int p0 = i * g.bs, p1 = min(p0 + g.bs, g.C);
-  const __nv_bfloat16* src = q + ((long long)b * g.C + p0) * g.q_stride + (long long)h * g.d + e;
-  float acc = 0.f;
-  for (int p = p0; p < p1; ++p, src += g.q_stride) acc += __bfloat162float(*src);
-  const float mean = acc / float(p1 - p0);
-  const __nv_bfloat16 hi = __float2bfloat16_rn(mean);
-  const __nv_bfloat16 lo = __float2bfloat16_rn(mean - __bfloat162float(hi));
+  const int nq = (p1 - p0 + 3) / 4;
+  const int a0 = p0 + quarter * nq, a1 = min(a0 + nq, p1);
+  const uint4* src = reinterpret_cast<const uint4*>(q + (long long)b * g.C * g.q_stride + x0);
+  const long long stride = g.q_stride / 8;  // uint4 per token
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  auto add = [&](const uint4& w) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      acc[2 * c] += __uint_as_float(ws[c] << 16);
+      acc[2 * c + 1] += __uint_as_float(ws[c] & 0xffff0000u);
+    }
+  };
+  int p = a0;
+  for (; p + 8 <= a1; p += 8) {
+    uint4 w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = __ldg(src + (long long)(p + u) * stride);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) add(w[u]);
+  }
+  for (; p < a1; ++p) add(__ldg(src + (long long)p * stride));
+  if (quarter > 0) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) part[quarter - 1][st][c] = acc[c];
+  }
+  __syncthreads();
+  if (quarter != 0) return;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] += part[k][st][c];
+  const int h = x0 / g.d, e = x0 % g.d;
+  const float inv = 1.0f / float(p1 - p0);
+  uint32_t hi[4], lo[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float m0 = acc[2 * c] * inv, m1 = acc[2 * c + 1] * inv;
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(m0), h1 = __float2bfloat16_rn(m1);
+    hi[c] = pack_bf16x2(__bfloat162float(h0), __bfloat162float(h1));
+    lo[c] = pack_bf16x2(m0 - __bfloat162float(h0), m1 - __bfloat162float(h1));
+  }
   const int grp = h / g.E, hl = h % g.E;
   const long long row = ((long long)b * g.Gn + grp) * g.Rpad + hl * g.nqb + i;
   const long long nrows = (long long)g.B * g.Gn * g.Rpad;
-  qbar[row * g.d + e] = hi;
-  qbar[(nrows + row) * g.d + e] = lo;
+  *reinterpret_cast<uint4*>(qbar + row * g.d + e) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4*>(qbar + (nrows + row) * g.d + e) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   if (e == 0) mstar_key[row] = float_key(-INFINITY);
 }
 
@@ -100,41 +142,47 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      const int row0 = bg * g.Rpad + rt * 128;
-      const int nrows = g.B * g.Gn * g.Rpad;
+  // TMA / MMA roles: whole warp runs the loop (warp-uniform values live in uniform registers),
+  // one elected lane issues each TMA / tcgen05 instruction.
+  if (warp == 0) {  // ---------------- TMA producer
+    const int row0 = bg * g.Rpad + rt * 128;
+    const int nrows = g.B * g.Gn * g.Rpad;
+    if (elect_one()) {
       mbar_expect_tx(bar_a, 2 * Cfg::kABytes);
 #pragma unroll
       for (int a = 0; a < Cfg::kAtoms; ++a) {
         tma_load_2d(sA_hi + a * 128 * 128, &tm_qbar, bar_a, 64 * a, row0);
         tma_load_2d(sA_lo + a * 128 * 128, &tm_qbar, bar_a, 64 * a, nrows + row0);
       }
-      const uint64_t pol = l2_policy_evict_first();
-      for (int n = 0; n < n_pages; ++n) {
-        const int s = n % Cfg::kStages;
-        mbar_wait(empty + s, ((n / Cfg::kStages) & 1) ^ 1);
-        const int page = __ldg(page_table + (long long)b * g.maxb + j0 + n);
-        uint8_t* dst = sK + s * Cfg::kKBytes;
+    }
+    __syncwarp();
+    const uint64_t pol = l2_policy_evict_first();
+    for (int n = 0; n < n_pages; ++n) {
+      const int s = n % Cfg::kStages;
+      const int page = __ldg(page_table + (long long)b * g.maxb + j0 + n);
+      mbar_wait(empty + s, ((n / Cfg::kStages) & 1) ^ 1);
+      uint8_t* dst = sK + s * Cfg::kKBytes;
+      if (elect_one()) {
         mbar_expect_tx(full + s, Cfg::kKBytes);
 #pragma unroll
         for (int a = 0; a < Cfg::kAtoms; ++a)
           tma_load_4d_hint(dst + a * BS * 128, &tm_k, full + s, 64 * a, 0, kvh, page, pol);
       }
+      __syncwarp();
     }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      constexpr uint32_t idesc = umma_idesc_bf16(128, BS, 0, 0);
-      mbar_wait(bar_a, 0);
+  } else if (warp == 1) {  // ---------------- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(128, BS, 0, 0);
+    mbar_wait(bar_a, 0);
+    tc_fence_after();
+    const uint32_t a_hi = smem_u32(sA_hi), a_lo = smem_u32(sA_lo);
+    for (int n = 0; n < n_pages; ++n) {
+      const int s = n % Cfg::kStages, acc = n & 1;
+      mbar_wait(full + s, (n / Cfg::kStages) & 1);
+      mbar_wait(acc_empty + acc, ((n >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t a_hi = smem_u32(sA_hi), a_lo = smem_u32(sA_lo);
-      for (int n = 0; n < n_pages; ++n) {
-        const int s = n % Cfg::kStages, acc = n & 1;
-        mbar_wait(full + s, (n / Cfg::kStages) & 1);
-        mbar_wait(acc_empty + acc, ((n >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t kb = smem_u32(sK + s * Cfg::kKBytes);
-        const uint32_t d_tm = tmem + acc * BS;
+      const uint32_t kb = smem_u32(sK + s * Cfg::kKBytes);
+      const uint32_t d_tm = tmem + acc * BS;
+      if (elect_one()) {
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           const uint32_t abase = half ? a_lo : a_hi;
@@ -150,6 +198,7 @@ __global__ void __launch_bounds__(192, 1)
         tc_commit(empty + s);
         tc_commit(acc_full + acc);
       }
+      __syncwarp();
     }
   } else {  // ---------------- epilogue: warps 2..5, one accumulator row per thread
     const int quarter = warp & 3;
@@ -219,7 +268,7 @@ int score_smem_bytes(int d, int bs) {
 
 cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
                           cudaStream_t st, int* launches) {
-  k_pool_q<<<dim3(g.nqb, g.Hq, g.B), g.d, 0, st>>>(q, g, qbar, mstar_key);
+  k_pool_q<<<dim3(g.nqb, g.B, (g.Hq * g.d) / 512), 256, 0, st>>>(q, g, qbar, mstar_key);
   ++*launches;
   if (g.Rpad > g.R) {
     const long long total = (long long)g.B * g.Gn * (g.Rpad - g.R) * g.d;

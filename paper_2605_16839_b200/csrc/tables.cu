@@ -35,14 +35,20 @@ __global__ void __launch_bounds__(128)
     } else {
       const float mstar = key_float(__ldg(mstar_key + (long long)bg * g.Rpad + r));
       const int jmax = g.pb + i;  // causal-valid blocks j <= pb + i
-      bits = 0;
-#pragma unroll 8
+      // all 32 loads first (each a coalesced 128 B warp request), then the threshold
+      float mv[32];
+#pragma unroll
       for (int jj = 0; jj < 32; ++jj) {
         const int j = jbase + jj;
-        if (j > jmax || j >= g.nkvb) break;
-        const float m = __ldg(scores + ((long long)bg * g.nkvb + j) * g.Rpad + r);
-        const bool keep = (m - mstar >= g.ln_alpha) || (j >= g.pb) || (sink && j == 0);
-        bits |= (uint32_t)keep << jj;
+        mv[jj] = (j <= jmax && j < g.nkvb) ? __ldg(scores + ((long long)bg * g.nkvb + j) * g.Rpad + r) : -INFINITY;
+      }
+      bits = 0;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) {
+        const int j = jbase + jj;
+        const bool valid = j <= jmax && j < g.nkvb;
+        const bool keep = (mv[jj] - mstar >= g.ln_alpha) || (j >= g.pb) || (sink && j == 0);
+        bits |= (uint32_t)(valid && keep) << jj;
       }
       if (mask_out != nullptr) mask_out[mw] = bits;
     }
