@@ -161,9 +161,25 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CPA_BENCH_ONE_DEVICE=1 (test only): every rank on cuda:0 with a gloo group, to exercise the
+    # sharded code path on a single-GPU box; real runs use one GPU per rank and NCCL.
+    one_dev = os.environ.get("CPA_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
+    backend = "gloo" if one_dev else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def max_over_ranks(vals):
+        if world == 1:
+            return vals
+        t = torch.tensor(vals, dtype=torch.float64, device="cpu" if one_dev else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(x) for x in t.tolist()]
     cfg = CONFIGS[args.config]
     seed = seed_of(args.config)
     P, C, L = cfg.chunk_geometry()
@@ -221,11 +237,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    ms = float(np.mean(ts))
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks([float(np.mean(ts))])[0]
 
     # ---- stage breakdown and the dense baseline (same kernels, tables = all blocks)
     reps = max(3, min(args.steps, 10))
@@ -259,10 +271,7 @@ def run_gpu(args):
     e2e_ms = float(np.mean(timed(e2e_step, args.steps, 1)))
     h2d = (dq.numel() + kc.numel() + vc.numel()) * 2
     d2h = o.numel() * 2
-    if world > 1:
-        t = torch.tensor([e2e_ms, t_attn, t_dense, t_tables], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms, t_attn, t_dense, t_tables = [float(x) for x in t.tolist()]
+    e2e_ms, t_attn, t_dense, t_tables = max_over_ranks([e2e_ms, t_attn, t_dense, t_tables])
 
     peak_tf, peak_bw, peak_src = peaks()
     achieved_tf = f_sel / (t_attn * 1e-3) / 1e12
@@ -284,7 +293,7 @@ def run_gpu(args):
             "config": {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk,
                        "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": d,
                        "block_size": bs, "alpha": ALPHA, "needle_density": RHO,
-                       "parallelism": f"kv-group shard x{world}" + (" + NCCL all-gather" if world > 1 else ""),
+                       "parallelism": f"kv-group shard x{world}" + (f" + {backend} all-gather" if world > 1 else ""),
                        "l2": "flushed (512 MiB write) before every timed step"},
             "dense_ms_per_chunk": round(t_dense, 4),
             "speedup_vs_dense": round(t_dense / ms, 3),

@@ -23,9 +23,10 @@ __global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict_
   const int i = blockIdx.x, b = blockIdx.y;
   const int st = threadIdx.x & 63, quarter = threadIdx.x >> 6;
   const int x0 = (blockIdx.z * 64 + st) * 8;  // element offset in [0, Hq*d)
+  const bool active = x0 < g.Hq * g.d;         // last slab may be partial (Hq*d % 512 != 0)
   const int p0 = i * g.bs, p1 = min(p0 + g.bs, g.C);
   const int nq = (p1 - p0 + 3) / 4;
-  const int a0 = p0 + quarter * nq, a1 = min(a0 + nq, p1);
+  const int a0 = p0 + quarter * nq, a1 = active ? min(a0 + nq, p1) : a0;
   const uint4* src = reinterpret_cast<const uint4*>(q + (long long)b * g.C * g.q_stride + x0);
   const long long stride = g.q_stride / 8;  // uint4 per token
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict_
     for (int c = 0; c < 8; ++c) part[quarter - 1][st][c] = acc[c];
   }
   __syncthreads();
-  if (quarter != 0) return;
+  if (quarter != 0 || !active) return;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -268,7 +269,7 @@ int score_smem_bytes(int d, int bs) {
 
 cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
                           cudaStream_t st, int* launches) {
-  k_pool_q<<<dim3(g.nqb, g.B, (g.Hq * g.d) / 512), 256, 0, st>>>(q, g, qbar, mstar_key);
+  k_pool_q<<<dim3(g.nqb, g.B, (g.Hq * g.d + 511) / 512), 256, 0, st>>>(q, g, qbar, mstar_key);
   ++*launches;
   if (g.Rpad > g.R) {
     const long long total = (long long)g.B * g.Gn * (g.Rpad - g.R) * g.d;

@@ -30,9 +30,10 @@ def allgather_heads(o_local: torch.Tensor, out: torch.Tensor | None = None, grou
         out = torch.empty((world,) + tuple(o_local.shape), dtype=o_local.dtype, device=o_local.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, o_local.contiguous(), group=group)
-    else:
-        parts = list(out.unbind(0))
-        dist.all_gather(parts, o_local.contiguous(), group=group)
+    else:  # gloo (CPU tests, single-device bench smoke): gather through host memory
+        host = [torch.empty(tuple(o_local.shape), dtype=o_local.dtype) for _ in range(world)]
+        dist.all_gather(host, o_local.detach().cpu(), group=group)
+        out.copy_(torch.stack(host))
     return out
 
 

@@ -295,3 +295,12 @@ def test_full_size_sampled(cfg_name, n_rows):
     got = o.float().cpu().numpy()
     sel = tuple(np.array(rows).T)
     assert rel_err(got[sel], ref[sel]) <= ATOL_REL
+
+
+@pytest.mark.parametrize("Hq,Hkv,E,d", [(4, 1, 4, 64), (8, 1, 4, 128), (2, 2, 1, 64)])
+def test_estimator_odd_head_counts(Hq, Hkv, E, d):
+    # Hq*d not a multiple of 512 (partial pool_q slab), sub-KV-group E < Hq/Hkv, MHA
+    q, k, v = random_qkv(1, Hq, Hkv, d, 96, 96 + 256, seed=Hq * 10 + d)
+    case = Case(q, k, v, 256, 32, alpha=0.06, E=E, seed=4)
+    ndiff, _, _ = _check_estimator(case)
+    assert ndiff <= 2
