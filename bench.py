@@ -67,6 +67,23 @@ def attention_flops(indptr, indices, C, P, bs, E, d):
     return 4 * d * E * total
 
 
+def sparsity_report(bits, nkvb, pb, nqb, Hq, E_exec, E_kv):
+    """Per-stage prefix sparsity (fraction of causal-valid PREFIX block slots not selected; the
+    forced chunk blocks excluded, R14) from the GPU's mask bits [B, Hq, nqb, nwords]:
+    pre-union, Q-block union, execution-group union, full-KV-group union."""
+    b64 = bits.view(np.uint32).astype(np.uint64)
+    B = b64.shape[0]
+    M = ((b64[..., None] >> np.arange(32, dtype=np.uint64)) & 1).astype(bool).reshape(B, Hq, nqb, -1)[..., :pb]
+    Mbar = M.any(axis=2)                                   # [B, Hq, pb]
+    Gx = Mbar.reshape(B, Hq // E_exec, E_exec, pb).any(axis=2)
+    Gk = Mbar.reshape(B, Hq // E_kv, E_kv, pb).any(axis=2)
+    n = B * Hq * nqb * pb
+    return {"pre_union": round(1 - M.sum() / n, 4),
+            "q_block_union": round(1 - Mbar.sum() * nqb / n, 4),
+            "exec_group_union": round(1 - np.repeat(Gx, E_exec, axis=1).sum() * nqb / n, 4),
+            "kv_group_union": round(1 - np.repeat(Gk, E_kv, axis=1).sum() * nqb / n, 4)}
+
+
 # ------------------------------------------------------------------------------ clocks
 class ClockSampler:
     def __init__(self, device_index=0):
@@ -197,7 +214,8 @@ def run_gpu(args):
     dq = dev(q)
     kc = dev(k[:, :, P:].transpose(0, 2, 1, 3))  # the chunk's own K/V [B, C, Hkv, d] (re-appended)
     vc = dev(v[:, :, P:].transpose(0, 2, 1, 3))
-    p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA)
+    E_exec = args.exec_group or E
+    p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group)
     tables = cpa.alloc_tables(p)
     ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
     o = torch.empty(cfg.batch, C, hq_l, d, dtype=torch.bfloat16, device="cuda")
@@ -248,10 +266,18 @@ def run_gpu(args):
     t_append = float(np.mean(timed(lambda: cpa.append_kv(p, kc, vc, cache), reps, 1)))
     ip = tables.kv_indptr.cpu().numpy()
     ix = tables.kv_indices.cpu().numpy()[: ip[-1]]
-    f_sel = attention_flops(ip, ix, C, P, bs, E, d)
-    all_ip = np.arange(cfg.batch * (hq_l // E) + 1) * nkvb
-    f_dense = attention_flops(all_ip, np.tile(np.arange(nkvb), cfg.batch * (hq_l // E)), C, P, bs, E, d)
-    density = (ip[-1] - cfg.batch * (hq_l // E) * (nkvb - P // bs)) / (cfg.batch * (hq_l // E) * (P // bs))
+    Gx = hq_l // E_exec
+    f_sel = attention_flops(ip, ix, C, P, bs, E_exec, d)
+    all_ip = np.arange(cfg.batch * Gx + 1) * nkvb
+    f_dense = attention_flops(all_ip, np.tile(np.arange(nkvb), cfg.batch * Gx), C, P, bs, E_exec, d)
+    density = (ip[-1] - cfg.batch * Gx * (nkvb - P // bs)) / (cfg.batch * Gx * (P // bs))
+    # per-stage sparsity from the GPU's own mask bits (one extra build, outside the timed region)
+    pm = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
+                         flags=cpa.F_MASK_OUT)
+    tm = cpa.alloc_tables(pm, mask=True)
+    cpa.build_tables(pm, dq, cache, tm)
+    nqb = -(-C // bs)
+    sparsity = sparsity_report(tm.mask_bits.cpu().numpy(), nkvb, P // bs, nqb, hq_l, E_exec, E)
 
     # ---- e2e: the same step through the public API with HOST buffers (pinned), copies timed
     hq_pin = dq.cpu().pin_memory()
@@ -292,7 +318,7 @@ def run_gpu(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk,
                        "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": d,
-                       "block_size": bs, "alpha": ALPHA, "needle_density": RHO,
+                       "block_size": bs, "alpha": ALPHA, "needle_density": RHO, "exec_group_size": E_exec,
                        "parallelism": f"kv-group shard x{world}" + (f" + {backend} all-gather" if world > 1 else ""),
                        "l2": "flushed (512 MiB write) before every timed step"},
             "dense_ms_per_chunk": round(t_dense, 4),
@@ -301,6 +327,7 @@ def run_gpu(args):
             "stage_ms": {"append": round(t_append, 4), "estimator+tables": round(t_tables, 4),
                          "attention": round(t_attn, 4)},
             "tabled_prefix_density": round(float(density), 4),
+            "sparsity": sparsity,
             "effective_tflops": round(f_dense / (ms * 1e-3) / 1e12, 1),
             "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
@@ -354,6 +381,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="llama8b_128k", choices=[c for c in CONFIGS if c != "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--exec-group", type=int, default=0,
+                    help="execution-group size E (0 = full KV group; 4 = sub-KV-group union, PAPER.md:498)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -11,14 +11,15 @@ Q/K/V (PAPER.md:262-263 names the model; 32 q heads / 8 KV heads / d=128 are its
 public shape) with N(0,1) background and planted "needle" KV blocks, so the
 estimator's masks are non-trivial (BASELINE.json north_star: "random data, with
 planted high-score 'needle' blocks").
-  * per (b, KV group) an orthonormal topic basis U (d x 12);
+  * per (b, KV group) an orthonormal topic basis U (d x 3E, E = Hq/Hkv: 12 topics for GQA 4);
   * background q, k projected onto U-perp (no topic cross-talk), v ~ N(0,1);
   * n_N = round(rho * (pb_max - 1)) needle blocks drawn without replacement
     from prefix blocks [1, pb_max); each gets a topic c and all its keys get
     +beta_k * u_c;
   * query head h (local index hl within its group) has topic pool
-    {(3*hl + t) mod 12 : t < 6}; each (h, q-block) draws s=4 pool topics and all
-    its queries get +beta_q * sum u_c;
+    {(3*hl + t) mod 3E : t < 6}; each (h, q-block) draws s=4 pool topics and all
+    its queries get +beta_q * sum u_c (for GQA 8 the two 4-head sub-groups cover
+    overlapping but different topic sets, so sub-KV-group union keeps fewer blocks);
   * beta_q * beta_k / sqrt(d) = 6 (needle pooled logit ~ 6 vs background ~0.3).
 Random numbers come from numpy Philox keyed by (seed, tensor, b, head, chunk), so
 any slice (one KV head for one rank, one chunk's Q) regenerates identically.
@@ -71,6 +72,9 @@ CONFIGS = {
     "llama8b_32k": Config("llama8b_32k", 1, 32, 8, 128, 128, 32768, 2048),
     "llama8b_128k": Config("llama8b_128k", 1, 32, 8, 128, 128, 131072, 4096),
     "llama8b_64k_b4": Config("llama8b_64k_b4", 4, 32, 8, 128, 128, 65536, 2048),
+    # NEXT-2: GQA 8:1 (Qwen3-30B-A3B attention shape: 32 q / 4 KV heads, d=128;
+    # PAPER.md:673-699), run with sub-KV-group union (exec_group_size=4)
+    "qwen3_30b_128k": Config("qwen3_30b_128k", 1, 32, 4, 128, 128, 131072, 4096),
 }
 
 
@@ -89,11 +93,15 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     return (u.astype(np.uint32)).view(np.float32)
 
 
-def _topics(seed: int, b: int, g: int, d: int) -> np.ndarray:
-    rng = _key(seed, "topics", b, g)
-    a = rng.standard_normal((d, N_TOPICS))
+def n_topics(cfg: "Config") -> int:
+    return 3 * cfg.group_size if cfg.group_size > 4 else N_TOPICS
+
+
+def _topics(seed: int, b: int, g: int, d: int, nt: int = N_TOPICS) -> np.ndarray:
+    rng = _key(seed, "topics", b, g) if nt == N_TOPICS else _key(seed, "topics", b, g, nt)
+    a = rng.standard_normal((d, nt))
     qmat, _ = np.linalg.qr(a)
-    return qmat.astype(np.float32)  # d x 12, orthonormal columns
+    return qmat.astype(np.float32)  # d x nt, orthonormal columns
 
 
 def needle_plan(cfg: Config, seed: int, rho: float, b: int, g: int):
@@ -104,7 +112,7 @@ def needle_plan(cfg: Config, seed: int, rho: float, b: int, g: int):
     n_n = int(round(rho * n_cand))
     rng = _key(seed, "plan", b, g)
     blocks = np.sort(rng.choice(np.arange(1, pb_max), size=n_n, replace=False)) if n_n > 0 else np.zeros(0, np.int64)
-    topics = rng.integers(0, N_TOPICS, size=n_n)
+    topics = rng.integers(0, n_topics(cfg), size=n_n)
     return blocks, topics
 
 
@@ -128,7 +136,7 @@ def make_kv(cfg: Config, seed: int, rho: float = 0.30, length: Optional[int] = N
             kk = rng.standard_normal((L, d), dtype=np.float32)
             vv = rng.standard_normal((L, d), dtype=np.float32)
             if needles:
-                U = _topics(seed, b, g, d)
+                U = _topics(seed, b, g, d, n_topics(cfg))
                 kk -= (kk @ U) @ U.T
                 blocks, topics = needle_plan(cfg, seed, rho, b, g)
                 bs = cfg.block_size
@@ -156,9 +164,10 @@ def make_q(cfg: Config, seed: int, chunk_index: Optional[int] = None,
             qq = rng.standard_normal((C, d), dtype=np.float32)
             if needles:
                 g, hl = h // E, h % E
-                U = _topics(seed, b, g, d)
+                nt = n_topics(cfg)
+                U = _topics(seed, b, g, d, nt)
                 qq -= (qq @ U) @ U.T
-                pool = [(3 * hl + s) % N_TOPICS for s in range(TOPICS_PER_POOL)]
+                pool = [(3 * hl + s) % nt for s in range(TOPICS_PER_POOL)]
                 nqb = -(-C // bs)
                 for i in range(nqb):
                     sel = rng.choice(pool, size=TOPICS_PER_QBLOCK, replace=False)
