@@ -215,7 +215,8 @@ def run_gpu(args):
     kc = dev(k[:, :, P:].transpose(0, 2, 1, 3))  # the chunk's own K/V [B, C, Hkv, d] (re-appended)
     vc = dev(v[:, :, P:].transpose(0, 2, 1, 3))
     E_exec = args.exec_group or E
-    p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group)
+    p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
+                        flags=cpa.F_EXACT_SCORES if args.exact_scores else 0)
     tables = cpa.alloc_tables(p)
     ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
     o = torch.empty(cfg.batch, C, hq_l, d, dtype=torch.bfloat16, device="cuda")
@@ -273,7 +274,7 @@ def run_gpu(args):
     density = (ip[-1] - cfg.batch * Gx * (nkvb - P // bs)) / (cfg.batch * Gx * (P // bs))
     # per-stage sparsity from the GPU's own mask bits (one extra build, outside the timed region)
     pm = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
-                         flags=cpa.F_MASK_OUT)
+                         flags=cpa.F_MASK_OUT | (cpa.F_EXACT_SCORES if args.exact_scores else 0))
     tm = cpa.alloc_tables(pm, mask=True)
     cpa.build_tables(pm, dq, cache, tm)
     nqb = -(-C // bs)
@@ -319,6 +320,7 @@ def run_gpu(args):
             "config": {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk,
                        "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": d,
                        "block_size": bs, "alpha": ALPHA, "needle_density": RHO, "exec_group_size": E_exec,
+                       "scorer": "exact tile max (SPEC.md:223)" if args.exact_scores else "pooled query (SPEC.md:269)",
                        "parallelism": f"kv-group shard x{world}" + (f" + {backend} all-gather" if world > 1 else ""),
                        "l2": "flushed (512 MiB write) before every timed step"},
             "dense_ms_per_chunk": round(t_dense, 4),
@@ -381,6 +383,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="llama8b_128k", choices=[c for c in CONFIGS if c != "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--exact-scores", action="store_true", help="NEXT-1: SPEC's exact tile-max scorer")
     ap.add_argument("--exec-group", type=int, default=0,
                     help="execution-group size E (0 = full KV group; 4 = sub-KV-group union, PAPER.md:498)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -74,6 +74,8 @@ enum {
   CPA_F_MASK_OUT = 4u,    /* also write M to tables->mask_bits */
   CPA_F_SCORES_OUT = 8u,  /* also write block scores / row max to tables->scores / ->row_max */
   CPA_F_OUT_F32 = 16u,    /* O is fp32 instead of bf16 (parity/debug) */
+  CPA_F_EXACT_SCORES = 32u, /* SPEC.md:223 exact tile-max scorer (full QK^T, max over every causal
+                               (p, t) pair of the tile) instead of the pooled-query estimator */
   CPA_F_P_BF16 = 256u,    /* ablation: round softmax P to bf16 instead of fp16 before P.V (K3) */
   CPA_F_NO_2CTA = 512u    /* ablation: single-CTA attention kernel instead of the cta_group::2 pair */
 };

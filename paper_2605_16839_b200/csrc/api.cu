@@ -17,6 +17,9 @@ cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* q
 cudaError_t launch_block_scores(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
                                 const Geo& g, float* scores, int* mstar_key, int num_sms,
                                 cudaStream_t st, int* launches);
+cudaError_t launch_block_scores_exact(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
+                                      const Geo& g, float* scores, int* mstar_key, int num_sms, cudaStream_t st,
+                                      int* launches);
 cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& g,
                           const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
                           int* dev_status, int32_t* indptr, int32_t* indices, cudaStream_t st,
@@ -241,10 +244,18 @@ int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cp
     int s;
     if ((s = make_map(&tq, w.qbar, 2, dims, str, box, "qbar")) != CPA_OK) return s;
     if ((s = kv_map(&tk, c->k_pages, g, c->num_pages, ps, hs, "k")) != CPA_OK) return s;
-    if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(q), g, w.qbar, w.mstar_key, st, launches)) != cudaSuccess)
-      return cuda_fail(e, "pool_q");
-    if ((e = launch_block_scores(tq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) != cudaSuccess)
-      return cuda_fail(e, "block_scores");
+    if (p->flags & CPA_F_EXACT_SCORES) {  // NEXT-1: SPEC's exact tile-max scorer (full QK^T)
+      CUtensorMap tqq;
+      if ((s = q_map(&tqq, q, g)) != CPA_OK) return s;
+      if ((e = launch_block_scores_exact(tqq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) !=
+          cudaSuccess)
+        return cuda_fail(e, "block_scores_exact");
+    } else {
+      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(q), g, w.qbar, w.mstar_key, st, launches)) != cudaSuccess)
+        return cuda_fail(e, "pool_q");
+      if ((e = launch_block_scores(tq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) != cudaSuccess)
+        return cuda_fail(e, "block_scores");
+    }
     if (p->flags & CPA_F_SCORES_OUT) {
       if ((e = launch_row_max(w.mstar_key, g, out->row_max, st, launches)) != cudaSuccess)
         return cuda_fail(e, "row_max");

@@ -258,6 +258,207 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+// ---------------------------------------------------------------- NEXT-1: exact tile-max scores
+// SPEC.md:223 (the spec's default scorer): m[b,h,i,j] = max over the causal pairs (p in q-block i,
+// t in block j, t <= P+p) of scale * q_p . k_t, i.e. the tile max of the full QK^T. CTA = (b, head h,
+// q-block i, split of the pages j <= pb+i); A = the q-block's bs x d query tile (TMA from q), B = each K
+// page; D = bs x bs fp32 in TMEM; epilogue: per-row masked max -> warp max -> CTA max (named barrier),
+// written in the same [B*Gn][nkvb][Rpad] score layout (row r = hl*nqb + i) as the pooled estimator.
+// Not the hot path: it costs a full QK^T (~half of dense attention); selected by CPA_F_EXACT_SCORES.
+template <int D, int BS>
+struct ExactCfg {
+  static constexpr int kAtoms = D / 64;
+  static constexpr int kStages = 4;
+  static constexpr int kQBytes = 128 * D * 2;
+  static constexpr int kKBytes = BS * D * 2;
+  static constexpr int kTmemCols = (2 * BS) <= 32 ? 32 : (2 * BS);
+  static constexpr int kSmem = kQBytes + kStages * kKBytes + 1024 + 256;
+};
+
+template <int D, int BS>
+__global__ void __launch_bounds__(192, 1)
+    k_block_scores_exact(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const int32_t* __restrict__ page_table, Geo g, int pages_per_cta,
+                         float* __restrict__ scores, int* __restrict__ mstar_key) {
+  using Cfg = ExactCfg<D, BS>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = smem + Cfg::kQBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sK + Cfg::kStages * Cfg::kKBytes);
+  uint64_t* bar_q = bars;
+  uint64_t* full = bars + 1;
+  uint64_t* empty = full + Cfg::kStages;
+  uint64_t* acc_full = empty + Cfg::kStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  __shared__ float wmax[4];
+
+  const int bh = blockIdx.z, b = bh / g.Hq, h = bh % g.Hq;
+  const int i = blockIdx.y;
+  const int jmax = g.pb + i;  // causal-valid blocks
+  const int j0 = blockIdx.x * pages_per_cta;
+  const int j1 = min(jmax + 1, j0 + pages_per_cta);
+  const int n_pages = j1 - j0;
+  if (n_pages <= 0) return;
+  const int grp = h / g.E, hl = h % g.E;
+  const int kvh = h / g.kv_per_q;
+  const int p0 = i * g.bs;  // q-block i = chunk positions [p0, p0 + bs)
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < Cfg::kStages; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(acc_full + s, 1); mbar_init(acc_empty + s, 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {  // ---------------- TMA producer (queries of the q-block: 128 rows, rows >= bs unused)
+    if (elect_one()) {
+      mbar_expect_tx(bar_q, Cfg::kQBytes);
+#pragma unroll
+      for (int a = 0; a < Cfg::kAtoms; ++a) tma_load_4d(sQ + a * 128 * 128, &tm_q, bar_q, 64 * a, h, p0, b);
+    }
+    __syncwarp();
+    for (int n = 0; n < n_pages; ++n) {
+      const int s = n % Cfg::kStages;
+      const int page = __ldg(page_table + (long long)b * g.maxb + j0 + n);
+      mbar_wait(empty + s, ((n / Cfg::kStages) & 1) ^ 1);
+      if (elect_one()) {
+        mbar_expect_tx(full + s, Cfg::kKBytes);
+#pragma unroll
+        for (int a = 0; a < Cfg::kAtoms; ++a)
+          tma_load_4d(sK + s * Cfg::kKBytes + a * BS * 128, &tm_k, full + s, 64 * a, 0, kvh, page);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {  // ---------------- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(128, BS, 0, 0);
+    mbar_wait(bar_q, 0);
+    tc_fence_after();
+    const uint32_t qa = smem_u32(sQ);
+    for (int n = 0; n < n_pages; ++n) {
+      const int s = n % Cfg::kStages, acc = n & 1;
+      mbar_wait(full + s, (n / Cfg::kStages) & 1);
+      mbar_wait(acc_empty + acc, ((n >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t kb = smem_u32(sK + s * Cfg::kKBytes);
+      if (elect_one()) {
+#pragma unroll
+        for (int a = 0; a < Cfg::kAtoms; ++a)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_ss(tmem + acc * BS, umma_desc_sw128(qa + a * 128 * 128 + kk * 32, 16, 1024),
+                   umma_desc_sw128(kb + a * BS * 128 + kk * 32, 16, 1024), idesc, (a | kk) != 0);
+        tc_commit(empty + s);
+        tc_commit(acc_full + acc);
+      }
+      __syncwarp();
+    }
+  } else {  // ---------------- epilogue: warps 2..5, one query row per thread
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const int p = p0 + row;
+    const bool valid = row < g.bs && p < g.C;
+    const int lim = valid ? g.P + p : -1;  // t <= P + p
+    const int r = hl * g.nqb + i;
+    const long long bg = (long long)b * g.Gn + grp;
+    float best = -INFINITY;
+    for (int n = 0; n < n_pages; ++n) {
+      const int acc = n & 1, j = j0 + n;
+      mbar_wait(acc_full + acc, (n >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + acc * BS;
+      const int tbase = j * g.bs;
+      float mx = -INFINITY;
+      if constexpr (BS >= 32) {
+#pragma unroll
+        for (int c0 = 0; c0 < BS; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(taddr + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (tbase + c0 + c <= lim) mx = fmaxf(mx, __uint_as_float(v[c]));
+        }
+      } else {
+        uint32_t v[16];
+        tmem_ld16(taddr, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < BS && tbase + c <= lim) mx = fmaxf(mx, __uint_as_float(v[c]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc_empty + acc);
+      // tile max over the 128 query rows: warp max on order-preserving int keys, then 4 warps
+      const int wk = __reduce_max_sync(0xffffffffu, float_key(mx));
+      if (lane == 0) wmax[quarter] = key_float(wk);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (row == 0) {
+        const float m = fmaxf(fmaxf(wmax[0], wmax[1]), fmaxf(wmax[2], wmax[3])) * g.scale;
+        scores[(bg * g.nkvb + j) * g.Rpad + r] = m;
+        best = fmaxf(best, m);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    if (row == 0) atomicMax(mstar_key + bg * g.Rpad + r, float_key(best));
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::kTmemCols>(tmem);
+  }
+}
+
+// scores / row-max initialisation for the exact scorer: every causal-invalid tile stays -inf
+__global__ void k_scores_init(Geo g, float* __restrict__ scores, int* __restrict__ mstar_key) {
+  const long long ns = (long long)g.B * g.Gn * g.nkvb * g.Rpad, nm = (long long)g.B * g.Gn * g.Rpad;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < ns; x += (long long)gridDim.x * blockDim.x) {
+    scores[x] = -INFINITY;
+    if (x < nm) mstar_key[x] = float_key(-INFINITY);
+  }
+}
+
+template <int D, int BS>
+static cudaError_t launch_exact_t(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt, const Geo& g,
+                                  float* scores, int* mstar_key, int num_sms, cudaStream_t st) {
+  using Cfg = ExactCfg<D, BS>;
+  auto kern = k_block_scores_exact<D, BS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+  if (e != cudaSuccess) return e;
+  const long long units = (long long)g.B * g.Hq * g.nqb;
+  int splits = (int)((2LL * num_sms + units - 1) / units);
+  if (splits < 1) splits = 1;
+  if (splits > g.nkvb) splits = g.nkvb;
+  const int ppc = (g.nkvb + splits - 1) / splits;
+  splits = (g.nkvb + ppc - 1) / ppc;
+  kern<<<dim3(splits, g.nqb, g.B * g.Hq), 192, Cfg::kSmem, st>>>(tq, tk, pt, g, ppc, scores, mstar_key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_block_scores_exact(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
+                                      const Geo& g, float* scores, int* mstar_key, int num_sms, cudaStream_t st,
+                                      int* launches) {
+  k_scores_init<<<1024, 256, 0, st>>>(g, scores, mstar_key);
+  *launches += 2;
+#define CPA_SC(DD, BB) \
+  if (g.d == DD && g.bs == BB) return launch_exact_t<DD, BB>(tq, tk, pt, g, scores, mstar_key, num_sms, st);
+  CPA_SC(64, 16) CPA_SC(64, 32) CPA_SC(64, 64) CPA_SC(64, 128)
+  CPA_SC(128, 16) CPA_SC(128, 32) CPA_SC(128, 64) CPA_SC(128, 128)
+#undef CPA_SC
+  return cudaErrorInvalidValue;
+}
+
 // ---------------------------------------------------------------- launchers
 int score_smem_bytes(int d, int bs) {
 #define CPA_SC(DD, BB) if (d == DD && bs == BB) return ScoreCfg<DD, BB>::kSmem;

@@ -89,13 +89,13 @@ def test_tables_wide_rows():
 
 # ----------------------------------------------------------------------------- a1-a3 estimator
 
-def _check_estimator(case: Case, sink=True):
+def _check_estimator(case: Case, sink=True, exact=False):
     p = case.params
-    p.flags |= cpa.F_SCORES_OUT | cpa.F_MASK_OUT
+    p.flags |= cpa.F_SCORES_OUT | cpa.F_MASK_OUT | (cpa.F_EXACT_SCORES if exact else 0)
     t = cpa.alloc_tables(p, mask=True, scores=True)
     cpa.build_tables(p, case.dq, case.cache, t)
     torch.cuda.synchronize()
-    m_ref = O.block_scores_pooled(case.q, case.k, case.P, case.bs)
+    m_ref = (O.block_scores_exact if exact else O.block_scores_pooled)(case.q, case.k, case.P, case.bs)
     m_gpu = scores_to_bhij(t.scores, p)
     fin = np.isfinite(m_ref)
     assert np.array_equal(fin, np.isfinite(m_gpu)), "causal pattern of scores"
@@ -305,3 +305,23 @@ def test_estimator_odd_head_counts(Hq, Hkv, E, d):
     case = Case(q, k, v, 256, 32, alpha=0.06, E=E, seed=4)
     ndiff, _, _ = _check_estimator(case)
     assert ndiff <= 2
+
+
+@pytest.mark.parametrize("d,bs,C,P", [(64, 16, 64, 448), (128, 128, 200, 384), (128, 64, 130, 256)])
+def test_estimator_exact_random(d, bs, C, P):
+    # NEXT-1: SPEC.md:223 exact tile-max scorer on the GPU vs the oracle's block_scores_exact
+    q, k, v = random_qkv(2, 8, 2, d, C, P + C, seed=d + bs + C + 1)
+    ndiff, _, _ = _check_estimator(Case(q, k, v, P, bs, alpha=0.06, seed=3), exact=True)
+    assert ndiff <= 2
+
+
+def test_exact_scorer_chunk_step_tiny_planted():
+    cfg = CONFIGS["tiny"]
+    k, v = make_kv(cfg, 16839)
+    q = make_q(cfg, 16839)
+    P, C, L = cfg.chunk_geometry()
+    case = Case(q, k, v, P, cfg.block_size, seed=11, flags=cpa.F_EXACT_SCORES)
+    got, (ip, ix) = _chunk_step(case)
+    ref = O.chunk_step(q, k, v, P, cfg.block_size, alpha=0.06, scorer="exact")
+    assert np.array_equal(ip, ref["indptr"]) and np.array_equal(ix, ref["indices"])
+    assert rel_err(got, ref["O"]) <= ATOL_REL
