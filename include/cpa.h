@@ -166,6 +166,15 @@ CPA_API int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chu
 CPA_API int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk,
                   const cpa_kv_cache* cache, void* stream);
 
+/* NEXT-3 execution ablation only ("CompactAttention-FP (Copy)"): gather the
+ * tabled K/V pages of every (b, g) row into a compact pool in `ws` (an explicit KV copy, exactly what
+ * the zero-copy path avoids), then run the same attention kernel over the compact pool through a
+ * per-row page table; causal masking stays in absolute positions (logical block ids are kept).
+ * Output equals cpa_paged_attention with the same tables. ws: cpa_copy_workspace_bytes(). */
+CPA_API size_t cpa_copy_workspace_bytes(const cpa_params* p);
+CPA_API int cpa_paged_attention_copy(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
+                                     const cpa_tables* tables, void* o, void* ws, size_t ws_bytes, void* stream);
+
 CPA_API const char* cpa_status_string(int status);
 CPA_API const char* cpa_last_error(void);  /* thread-local detail of the last failing call */
 CPA_API int cpa_version(void);

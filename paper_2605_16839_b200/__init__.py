@@ -17,6 +17,7 @@ import torch
 __all__ = [
     "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
     "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
+    "paged_attention_copy",
     "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "EXPORTED_SYMBOLS",
 ]
 
@@ -27,8 +28,8 @@ F_SINK, F_MASK_IN, F_MASK_OUT, F_SCORES_OUT, F_OUT_F32, F_EXACT_SCORES, F_P_BF16
 STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA_ERR_MISALIGNED",
           "CPA_ERR_ALPHA", "CPA_ERR_WORKSPACE", "CPA_ERR_CAPACITY", "CPA_ERR_CUDA"]
 EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",
-                    "cpa_append_kv", "cpa_status_string", "cpa_last_error", "cpa_version",
-                    "cpa_last_launch_count"]
+                    "cpa_append_kv", "cpa_copy_workspace_bytes", "cpa_paged_attention_copy",
+                    "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
 
 
 class CpaError(RuntimeError):
@@ -77,6 +78,11 @@ def lib() -> ctypes.CDLL:
         L.cpa_chunk_step.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(_Cache),
                                      ctypes.POINTER(_Tables), vp, vp, ctypes.c_size_t, vp]
         L.cpa_append_kv.argtypes = [ctypes.POINTER(Params), vp, vp, ctypes.POINTER(_Cache), vp]
+        L.cpa_copy_workspace_bytes.argtypes = [ctypes.POINTER(Params)]
+        L.cpa_copy_workspace_bytes.restype = ctypes.c_size_t
+        L.cpa_paged_attention_copy.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache),
+                                               ctypes.POINTER(_Tables), vp, vp, ctypes.c_size_t, vp]
+        L.cpa_paged_attention_copy.restype = i32
         for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv):
             f.restype = i32
         L.cpa_status_string.argtypes = [i32]
@@ -213,6 +219,18 @@ def chunk_step(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTab
 def append_kv(p: Params, k_chunk: torch.Tensor, v_chunk: torch.Tensor, cache: PagedKVCache, stream=None):
     c = cache._c()
     _check(lib().cpa_append_kv(ctypes.byref(p), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c), _stream(stream)))
+
+
+def paged_attention_copy(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables,
+                         out: torch.Tensor, workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """NEXT-3 ablation: gather the tabled pages into a compact pool, then attend (see cpa.h)."""
+    need = int(lib().cpa_copy_workspace_bytes(ctypes.byref(p)))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=q.device)
+    c, t = cache._c(), tables._c()
+    _check(lib().cpa_paged_attention_copy(ctypes.byref(p), _ptr(q), ctypes.byref(c), ctypes.byref(t), _ptr(out),
+                                          _ptr(workspace), workspace.numel(), _stream(stream)))
+    return out
 
 
 def last_launch_count() -> int:

@@ -38,6 +38,9 @@ cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap
                                         const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g,
                           long long page_stride, long long head_stride, cudaStream_t st, int* launches);
+cudaError_t launch_gather_pages(const cpa_kv_cache& c, const int32_t* indptr, const int32_t* indices, const Geo& g,
+                                long long ps, long long hs, void* ck, void* cv, int32_t* cpt, cudaStream_t st,
+                                int* launches);
 cudaError_t launch_row_max(const int* mstar_key, const Geo& g, float* row_max, cudaStream_t st,
                            int* launches);
 }  // namespace cpa
@@ -162,6 +165,7 @@ int make_geo(const cpa_params* p, Geo* g) {
   g->ln_alpha = logf(p->alpha);
   g->flags = p->flags;
   g->q_stride = qs;
+  g->b_stride = (long long)g->C * qs;
   return CPA_OK;
 }
 
@@ -205,7 +209,7 @@ WS carve(const Geo& g, void* base) {
 
 int q_map(CUtensorMap* m, const void* q, const Geo& g) {
   cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.Hq, (cuuint64_t)g.C, (cuuint64_t)g.B};
-  cuuint64_t str[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.q_stride * 2, (cuuint64_t)g.C * g.q_stride * 2};
+  cuuint64_t str[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.q_stride * 2, (cuuint64_t)g.b_stride * 2};
   cuuint32_t box[4] = {64, 1, 128, 1};
   return make_map(m, q, 4, dims, str, box, "q");
 }
@@ -271,32 +275,45 @@ int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cp
   return CPA_OK;
 }
 
-int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
-                   long long hs, const cpa_tables* t, void* o, cudaStream_t st) {
-  if (!q || !o) return fail(CPA_ERR_NULL, "q/o is NULL");
-  if (!aligned16(q) || !aligned16(o)) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
-  if (t && (!t->kv_indptr || !t->kv_indices)) return fail(CPA_ERR_NULL, "tables pointers");
+int attention_launch(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
+                     int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
+                     const int32_t* indices, void* o, cudaStream_t st) {
   CUtensorMap tq, tk, tv;
   int s;
   if ((s = q_map(&tq, q, g)) != CPA_OK) return s;
-  if ((s = kv_map(&tk, c->k_pages, g, c->num_pages, ps, hs, "k")) != CPA_OK) return s;
-  if ((s = kv_map(&tv, c->v_pages, g, c->num_pages, ps, hs, "v")) != CPA_OK) return s;
+  if ((s = kv_map(&tk, k_pages, g, num_pages, ps, hs, "k")) != CPA_OK) return s;
+  if ((s = kv_map(&tv, v_pages, g, num_pages, ps, hs, "v")) != CPA_OK) return s;
   AttnArgs a;
-  a.page_table = c->page_table;
-  a.indptr = t ? t->kv_indptr : nullptr;
-  a.indices = t ? t->kv_indices : nullptr;
+  a.page_table = page_table;
+  a.indptr = indptr;
+  a.indices = indices;
   a.out = o;
   a.out_f32 = (p->flags & CPA_F_OUT_F32) ? 1 : 0;
   cudaError_t e;
   if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA)) {
     CUtensorMap tkh;  // half a page of keys per CTA of the pair
-    if ((s = kv_map(&tkh, c->k_pages, g, c->num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
+    if ((s = kv_map(&tkh, k_pages, g, num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
     e = launch_paged_attention_2cta(tq, tkh, tv, g, a, st, &g_launches);
   } else {
     e = launch_paged_attention(tq, tk, tv, g, a, st, &g_launches);
   }
   if (e != cudaSuccess) return cuda_fail(e, "paged_attention");
   return CPA_OK;
+}
+
+int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
+                   long long hs, const cpa_tables* t, void* o, cudaStream_t st) {
+  if (!q || !o) return fail(CPA_ERR_NULL, "q/o is NULL");
+  if (!aligned16(q) || !aligned16(o)) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
+  if (t && (!t->kv_indptr || !t->kv_indices)) return fail(CPA_ERR_NULL, "tables pointers");
+  return attention_launch(p, g, q, c->k_pages, c->v_pages, c->num_pages, ps, hs, c->page_table,
+                          t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, st);
+}
+
+// NEXT-3 copy ablation: compact pool [B*Gn*nkvb pages] of K and of V + per-row page tables
+size_t copy_ws_bytes(const Geo& g) {
+  const size_t pages = (size_t)g.B * g.Gn * g.nkvb;
+  return 2 * up256(pages * g.bs * g.d * 2) + up256(pages * 4);
 }
 
 }  // namespace
@@ -378,6 +395,53 @@ int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chunk, cons
   g_launches = 0;
   if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream)) != CPA_OK) return s;
   g_launches += total;
+  return CPA_OK;
+}
+
+size_t cpa_copy_workspace_bytes(const cpa_params* p) {
+  Geo g;
+  if (make_geo(p, &g) != CPA_OK) return 0;
+  return copy_ws_bytes(g);
+}
+
+int cpa_paged_attention_copy(const cpa_params* p, const void* q, const cpa_kv_cache* cache, const cpa_tables* t,
+                             void* o, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  if (!q || !o || !t || !t->kv_indptr || !t->kv_indices) return fail(CPA_ERR_NULL, "q/o/tables NULL");
+  if (!ws || ws_bytes < copy_ws_bytes(g)) return fail(CPA_ERR_WORKSPACE, "copy workspace too small");
+  const size_t pages = (size_t)g.B * g.Gn * g.nkvb;
+  uint8_t* base = reinterpret_cast<uint8_t*>(ws);
+  void* ck = base;
+  void* cv = base + up256(pages * g.bs * g.d * 2);
+  int32_t* cpt = reinterpret_cast<int32_t*>(base + 2 * up256(pages * g.bs * g.d * 2));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = launch_gather_pages(*cache, t->kv_indptr, t->kv_indices, g, ps, hs, ck, cv, cpt, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "gather_pages");
+  // per batch entry: pseudo-batch over the Gn execution groups (one KV head each, its own page list)
+  for (int b = 0; b < g.B; ++b) {
+    Geo gb = g;
+    gb.B = g.Gn;
+    gb.Hq = g.E;
+    gb.Hkv = 1;
+    gb.Gn = 1;
+    gb.kv_per_q = g.E;
+    gb.b_stride = (long long)g.E * g.d;  // next group's heads
+    gb.maxb = g.nkvb;
+    gb.nwords = g.nwords;
+    const size_t off = (size_t)b * g.b_stride * 2;
+    const void* qb = reinterpret_cast<const uint8_t*>(q) + off;
+    void* ob = reinterpret_cast<uint8_t*>(o) + off * ((p->flags & CPA_F_OUT_F32) ? 2 : 1);
+    if ((s = attention_launch(p, gb, qb, ck, cv, (int)pages, (long long)g.bs * g.d, (long long)g.bs * g.d,
+                              cpt + (size_t)b * g.Gn * g.nkvb, t->kv_indptr + (size_t)b * g.Gn, t->kv_indices, ob,
+                              st)) != CPA_OK)
+      return s;
+  }
   return CPA_OK;
 }
 

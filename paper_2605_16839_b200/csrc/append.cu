@@ -38,6 +38,39 @@ cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c,
   return cudaGetLastError();
 }
 
+// NEXT-3 "copy" execution ablation: gather the tabled K/V pages of every
+// (b, g) row into a compact pool (slot e = the row's CSR entry) and write the row's page table
+// cpt[r][j] = e. grid (nkvb, B*Gn), 256 threads; CTA (x, r) copies entry indptr[r] + x if it exists.
+__global__ void __launch_bounds__(256) k_gather_pages(const uint4* __restrict__ kp, const uint4* __restrict__ vp,
+                                                      const int32_t* __restrict__ pt, const int32_t* __restrict__ indptr,
+                                                      const int32_t* __restrict__ indices, Geo g, long long ps,
+                                                      long long hs, uint4* __restrict__ ck, uint4* __restrict__ cv,
+                                                      int32_t* __restrict__ cpt) {
+  const int x = blockIdx.x, r = blockIdx.y;
+  const int beg = __ldg(indptr + r), len = __ldg(indptr + r + 1) - beg;
+  if (x >= len) return;
+  const int e = beg + x, j = __ldg(indices + e);
+  const int b = r / g.Gn, grp = r % g.Gn;
+  const int page = __ldg(pt + (long long)b * g.maxb + j);
+  const long long src = ((long long)page * ps + (long long)group_kv_head(g, grp) * hs) / 8;
+  const int nvec = g.bs * g.d / 8;
+  for (int t = threadIdx.x; t < nvec; t += blockDim.x) {
+    ck[(long long)e * nvec + t] = kp[src + t];
+    cv[(long long)e * nvec + t] = vp[src + t];
+  }
+  if (threadIdx.x == 0) cpt[(long long)r * g.nkvb + j] = e;
+}
+
+cudaError_t launch_gather_pages(const cpa_kv_cache& c, const int32_t* indptr, const int32_t* indices, const Geo& g,
+                                long long ps, long long hs, void* ck, void* cv, int32_t* cpt, cudaStream_t st,
+                                int* launches) {
+  k_gather_pages<<<dim3(g.nkvb, g.B * g.Gn), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(c.k_pages), reinterpret_cast<const uint4*>(c.v_pages), c.page_table, indptr,
+      indices, g, ps, hs, reinterpret_cast<uint4*>(ck), reinterpret_cast<uint4*>(cv), cpt);
+  ++*launches;
+  return cudaGetLastError();
+}
+
 __global__ void k_row_max(const int* __restrict__ key, long long n, float* __restrict__ out) {
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < n; x += (long long)gridDim.x * blockDim.x)
     out[x] = key_float(key[x]);

@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
       mbar_wait(o_full, 0);
       tc_fence_after();
     }
-    const long long obase = ((long long)b * g.C + p) * g.q_stride + (long long)h * D;
+    const long long obase = (long long)b * g.b_stride + (long long)p * g.q_stride + (long long)h * D;
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t o[32];

@@ -387,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tc_fence_after();
     }
     const uint32_t ob0 = tmem + lane_off + 256 + wg * (D / 2), ob1 = ob0 + 128;
-    const long long obase = ((long long)b * g.C + p) * g.q_stride + (long long)h * D + wg * (D / 2);
+    const long long obase = (long long)b * g.b_stride + (long long)p * g.q_stride + (long long)h * D + wg * (D / 2);
 #pragma unroll
     for (int cc = 0; cc < D / 2; cc += 32) {
       uint32_t o0[32], o1[32];

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict_
   const int p0 = i * g.bs, p1 = min(p0 + g.bs, g.C);
   const int nq = (p1 - p0 + 3) / 4;
   const int a0 = p0 + quarter * nq, a1 = active ? min(a0 + nq, p1) : a0;
-  const uint4* src = reinterpret_cast<const uint4*>(q + (long long)b * g.C * g.q_stride + x0);
+  const uint4* src = reinterpret_cast<const uint4*>(q + (long long)b * g.b_stride + x0);
   const long long stride = g.q_stride / 8;  // uint4 per token
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   auto add = [&](const uint4& w) {

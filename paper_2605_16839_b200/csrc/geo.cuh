@@ -14,6 +14,7 @@ struct Geo {
   float ln_alpha;
   uint32_t flags;
   long long q_stride;  // elements between tokens of q / o
+  long long b_stride;  // elements between batch entries of q / o (C*q_stride; other for pseudo-batches)
 };
 
 // KV head of execution group g: its query heads [g*E, (g+1)*E) all read KV head (g*E)/(Hq/Hkv).

@@ -325,3 +325,27 @@ def test_exact_scorer_chunk_step_tiny_planted():
     ref = O.chunk_step(q, k, v, P, cfg.block_size, alpha=0.06, scorer="exact")
     assert np.array_equal(ip, ref["indptr"]) and np.array_equal(ix, ref["indices"])
     assert rel_err(got, ref["O"]) <= ATOL_REL
+
+
+@pytest.mark.parametrize("d,bs,B", [(64, 16, 1), (128, 128, 2), (128, 64, 1)])
+def test_copy_ablation_matches_zero_copy(d, bs, B):
+    # NEXT-3: gather-then-attend must give exactly the zero-copy result
+    Hq, Hkv, C, P = 8, 2, 256, 8 * 128
+    q, k, v = random_qkv(B, Hq, Hkv, d, C, P + C, seed=d * bs + B)
+    case = Case(q, k, v, P, bs, seed=9)
+    nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+    M = random_block_mask(B, Hq, nqb, nkvb, 0.1, seed=bs + 1)
+    for i in range(nqb):
+        M[:, :, i, pb + i + 1:] = False
+        M[:, :, i, pb:pb + i + 1] = True
+    ip, ix = O.tables_from_mask(M, case.E, pb)
+    t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
+    p = case.params
+    p.flags |= cpa.F_OUT_F32
+    o1, o2 = case.out(True), case.out(True)
+    cpa.paged_attention(p, case.dq, case.cache, t, o1)
+    cpa.paged_attention_copy(p, case.dq, case.cache, t, o2)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    ref = O.paged_attention(q, k, v, P, bs, ip, ix)
+    assert rel_err(o2.cpu().numpy().astype(np.float64), ref) <= ATOL_REL
