@@ -262,7 +262,7 @@ def test_append_then_chunk_step_multi_chunk():
 
 
 @pytest.mark.parametrize("cfg_name,n_rows,E", [("llama8b_32k", 384, 0), ("llama8b_128k", 256, 0),
-                                                ("qwen3_30b_128k", 256, 4)])
+                                                ("qwen3_30b_128k", 256, 4), ("llama8b_64k_b4", 256, 0)])
 def test_full_size_sampled(cfg_name, n_rows, E):
     """BASELINE configs at full size: tables bit-exact vs the oracle (planted workload, margins > 2
     nats) and sampled output rows (incl. first/last tokens and every head) within tolerance, in the
@@ -349,3 +349,15 @@ def test_copy_ablation_matches_zero_copy(d, bs, B):
     assert torch.equal(o1, o2)
     ref = O.paged_attention(q, k, v, P, bs, ip, ix)
     assert rel_err(o2.cpu().numpy().astype(np.float64), ref) <= ATOL_REL
+
+
+@pytest.mark.parametrize("C,P,bs", [(1, 0, 16), (1, 256, 128), (17, 0, 32), (129, 128, 128), (5, 64, 64)])
+def test_chunk_step_edge_lengths(C, P, bs):
+    # single-token chunks, first chunk (P=0), chunk shorter than a block, one past a tile boundary
+    q, k, v = random_qkv(1, 8, 2, 128 if bs >= 64 else 64, C, P + C, seed=C * 7 + P + bs)
+    case = Case(q, k, v, P, bs, seed=2)
+    got, (ip, ix) = _chunk_step(case)
+    ref = O.chunk_step(q, k, v, P, bs, alpha=0.06)
+    nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+    assert ip[-1] >= 2 * (nkvb - pb)  # chunk blocks always tabled
+    assert rel_err(got, ref["O"]) <= ATOL_REL
