@@ -340,6 +340,49 @@ def paged_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, P: int, bs: int
     return out
 
 
+def expand_tables_to_mask(indptr, indices, B: int, Hq: int, E: int, C: int, P: int, bs: int) -> np.ndarray:
+    """q-uniform expansion of the block tables into a 2D per-(b,h,i) mask ("q-uniform
+    expansion of table"; PAPER.md:409 "the same unioned block mask"): Mq[b,h,i,j] = [j in T[b, h//E]]
+    for every q-block i, restricted to the causal-valid tiles j <= pb + i (SPEC.md:441 pre:
+    "mask causal-consistent"; SPEC.md:193)."""
+    nqb, nkvb, pb, _ = geometry(C, P, bs)
+    Gn = Hq // E
+    Mq = np.zeros((B, Hq, nqb, nkvb), dtype=bool)
+    for b in range(B):
+        for h in range(Hq):
+            r = b * Gn + h // E
+            for j in indices[indptr[r]:indptr[r + 1]]:
+                for i in range(nqb):
+                    if causal_valid(i, int(j), pb):
+                        Mq[b, h, i, j] = True
+    return Mq
+
+
+def block_sparse_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, P: int, bs: int,
+                           mask: np.ndarray, sm_scale: Optional[float] = None, rows=None) -> np.ndarray:
+    """Block-sparse execution of a 2D mask (the Fig. 7(c) baseline executor: "executes
+    this mask directly with a block-sparse kernel"; SPEC.md:440-449 exec_block_sparse): query p of
+    q-block i = p // bs under head h attends the tokens of the blocks {j : mask[b,h,i,j]} that are
+    causally visible, t <= P + p. Per-query-block rows, so the value differs from
+    the table executors unless the mask is q-uniform. An empty row raises.
+    Returns [B, C, Hq, d] float64 (`rows` as in paged_attention)."""
+    B, C, Hq, d = q.shape
+    _, Hkv, L, _ = k.shape
+    nqb, nkvb, pb, L2 = geometry(C, P, bs)
+    assert L == L2 and mask.shape == (B, Hq, nqb, nkvb)
+    scale = 1.0 / math.sqrt(d) if sm_scale is None else float(sm_scale)
+    out = np.full((B, C, Hq, d), np.nan)
+    if rows is None:
+        rows = [(b, p, h) for b in range(B) for h in range(Hq) for p in range(C)]
+    for (b, p, h) in rows:
+        i = p // bs
+        allowed = np.repeat(mask[b, h, i], bs)[:L].copy()
+        allowed[P + p + 1:] = False
+        kv = kv_head_of(h, Hq, Hkv)
+        out[b, p, h] = masked_attention_row(q[b, p, h], k[b, kv], v[b, kv], allowed, scale)
+    return out
+
+
 def dense_causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, P: int,
                            sm_scale: Optional[float] = None) -> np.ndarray:
     """Dense causal chunked attention: query p sees t <= P + p. fp64.

@@ -411,3 +411,61 @@ def test_chunk_step_end_to_end_tiny():
     nqb, nkvb, pb, _ = O.geometry(C, P, cfg.block_size)
     assert O.check_minimality(r["indptr"], r["indices"], r["M"], cfg.group_size, pb)
     assert np.isfinite(r["O"]).all()
+
+
+# ---- block-sparse executor (Fig. 7(c) baseline)
+
+def test_block_sparse_per_qblock_mask_equals_masked_sdpa():
+    # per-i distinct masks == masked dense attention with per-query allowed sets
+    B, Hq, Hkv, d, bs, P, C = 2, 4, 2, 16, 8, 48, 21
+    L = P + C
+    q, k, v = random_qkv(B, Hq, Hkv, d, C, L, seed=31)
+    nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+    M = random_block_mask(B, Hq, nqb, nkvb, 0.3, seed=31)
+    for i in range(nqb):
+        M[:, :, i, pb + i] = True  # the diagonal tile keeps every row non-empty
+    out = O.block_sparse_attention(q, k, v, P, bs, M)
+    allowed = torch.zeros(B, Hq, C, L, dtype=torch.bool)
+    Mt = torch.from_numpy(M)
+    for p in range(C):
+        allowed[:, :, p, :] = Mt[:, :, p // bs, :].repeat_interleave(bs, dim=-1)[..., :L]
+        allowed[:, :, p, P + p + 1:] = False
+    ref = _sdpa_fp64(q, k, v, P, allowed.numpy())
+    assert np.abs(out - ref).max() < 1e-12
+
+
+def test_block_sparse_full_mask_equals_dense():
+    # SPEC.md:448 "full mask -> equals dense oracle"
+    B, Hq, Hkv, d, bs, P, C = 1, 4, 1, 16, 8, 32, 17
+    q, k, v = random_qkv(B, Hq, Hkv, d, C, P + C, seed=32)
+    nqb, nkvb, _, _ = O.geometry(C, P, bs)
+    out = O.block_sparse_attention(q, k, v, P, bs, np.ones((B, Hq, nqb, nkvb), bool))
+    assert np.abs(out - O.dense_causal_attention(q, k, v, P)).max() < 1e-12
+
+
+def test_block_sparse_of_q_uniform_expansion_equals_tables():
+    # SPEC.md:447 + invariant SPEC.md:454: q-uniform expansion of the table == zero-copy executor
+    B, Hq, Hkv, d, bs, P, C = 2, 8, 2, 16, 8, 64, 24
+    q, k, v = random_qkv(B, Hq, Hkv, d, C, P + C, seed=33)
+    nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+    M = random_block_mask(B, Hq, nqb, nkvb, 0.15, seed=33)
+    M[..., pb:] = True
+    E = Hq // Hkv
+    indptr, indices = O.tables_from_mask(M, E, pb)
+    Mq = O.expand_tables_to_mask(indptr, indices, B, Hq, E, C, P, bs)
+    # the expansion is causal-consistent and lowers back to the same tables
+    for i in range(nqb):
+        assert not Mq[:, :, i, pb + i + 1:].any()
+    ip2, ix2 = O.tables_from_mask(Mq, E, pb)
+    assert np.array_equal(ip2, indptr) and np.array_equal(ix2, indices)
+    a = O.block_sparse_attention(q, k, v, P, bs, Mq)
+    b_ = O.paged_attention(q, k, v, P, bs, indptr, indices)
+    assert np.abs(a - b_).max() < 1e-12
+
+
+def test_block_sparse_empty_row_raises():
+    # empty row per (b,h,i) -> error
+    q, k, v = random_qkv(1, 2, 1, 8, 8, 16, seed=34)
+    M = np.zeros((1, 2, 1, 2), bool)
+    with pytest.raises(ValueError):
+        O.block_sparse_attention(q, k, v, 8, 8, M)
