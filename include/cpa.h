@@ -175,6 +175,24 @@ CPA_API size_t cpa_copy_workspace_bytes(const cpa_params* p);
 CPA_API int cpa_paged_attention_copy(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
                                      const cpa_tables* tables, void* o, void* ws, size_t ws_bytes, void* stream);
 
+/* NEXT-3 execution ablation only ("The block-sparse variant executes this mask directly
+ * with a block-sparse kernel"; SPEC.md:440-449 exec_block_sparse). Each (b, h, q-block i) tile runs
+ * over the KV blocks set in ITS OWN row of the 2D mask, one query head per CTA (no GQA sharing of the
+ * K/V tiles), the mask bits interpreted inside the kernel:
+ *   O[b,p,h] = sum_{t in A(p)} softmax_t(sm_scale q_p . k_t) v_t,
+ *   A(p) = { t : mask[b, h, p/bs, t/bs] = 1, t <= P + p }.
+ *   mask: u32 [B, Hq, nqb, nwords] device, layout of cpa_tables.mask_bits; bits j > pb + i are ignored.
+ *   A row whose A(p) is empty (SPEC.md:445 calls it an error) yields O = 0 for those queries.
+ * Requires block_size == 128 (one 128-query tile per q-block, FlashPrefill's block size)
+ * and nkvb <= 4096; otherwise CPA_ERR_UNSUPPORTED. ws is unused (may be NULL). */
+CPA_API int cpa_block_sparse_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
+                                       const uint32_t* mask, void* o, void* ws, size_t ws_bytes, void* stream);
+
+/* q-uniform expansion of tables into a 2D mask (the "same unioned block mask" of
+ * PAPER.md:409): mask[b,h,i,j] = [j in T[b, h/E]] && j <= pb + i, written for every (b, h, i).
+ * mask: u32 [B, Hq, nqb, nwords] device, overwritten. */
+CPA_API int cpa_expand_tables(const cpa_params* p, const cpa_tables* tables, uint32_t* mask, void* stream);
+
 CPA_API const char* cpa_status_string(int status);
 CPA_API const char* cpa_last_error(void);  /* thread-local detail of the last failing call */
 CPA_API int cpa_version(void);

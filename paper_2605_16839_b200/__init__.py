@@ -17,7 +17,7 @@ import torch
 __all__ = [
     "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
     "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
-    "paged_attention_copy",
+    "paged_attention_copy", "block_sparse_attention", "expand_tables",
     "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "EXPORTED_SYMBOLS",
 ]
 
@@ -29,7 +29,7 @@ STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA
           "CPA_ERR_ALPHA", "CPA_ERR_WORKSPACE", "CPA_ERR_CAPACITY", "CPA_ERR_CUDA"]
 EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",
                     "cpa_append_kv", "cpa_copy_workspace_bytes", "cpa_paged_attention_copy",
-                    "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
+                    "cpa_block_sparse_attention", "cpa_expand_tables", "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
 
 
 class CpaError(RuntimeError):
@@ -83,6 +83,11 @@ def lib() -> ctypes.CDLL:
         L.cpa_paged_attention_copy.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache),
                                                ctypes.POINTER(_Tables), vp, vp, ctypes.c_size_t, vp]
         L.cpa_paged_attention_copy.restype = i32
+        L.cpa_block_sparse_attention.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache), vp, vp, vp,
+                                                 ctypes.c_size_t, vp]
+        L.cpa_block_sparse_attention.restype = i32
+        L.cpa_expand_tables.argtypes = [ctypes.POINTER(Params), ctypes.POINTER(_Tables), vp, vp]
+        L.cpa_expand_tables.restype = i32
         for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv):
             f.restype = i32
         L.cpa_status_string.argtypes = [i32]
@@ -231,6 +236,22 @@ def paged_attention_copy(p: Params, q: torch.Tensor, cache: PagedKVCache, tables
     _check(lib().cpa_paged_attention_copy(ctypes.byref(p), _ptr(q), ctypes.byref(c), ctypes.byref(t), _ptr(out),
                                           _ptr(workspace), workspace.numel(), _stream(stream)))
     return out
+
+
+def block_sparse_attention(p: Params, q: torch.Tensor, cache: PagedKVCache, mask_bits: torch.Tensor,
+                           out: torch.Tensor, stream=None) -> torch.Tensor:
+    """NEXT-3 ablation: execute a 2D per-(b,h,q-block) mask [B,Hq,nqb,nwords] directly (see cpa.h)."""
+    c = cache._c()
+    _check(lib().cpa_block_sparse_attention(ctypes.byref(p), _ptr(q), ctypes.byref(c), _ptr(mask_bits), _ptr(out),
+                                            None, 0, _stream(stream)))
+    return out
+
+
+def expand_tables(p: Params, tables: BlockTables, mask_bits: torch.Tensor, stream=None) -> torch.Tensor:
+    """q-uniform expansion of the tables into a 2D mask [B,Hq,nqb,nwords] (see cpa.h)."""
+    t = tables._c()
+    _check(lib().cpa_expand_tables(ctypes.byref(p), ctypes.byref(t), _ptr(mask_bits), _stream(stream)))
+    return mask_bits
 
 
 def last_launch_count() -> int:

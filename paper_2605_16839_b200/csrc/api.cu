@@ -24,13 +24,6 @@ cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& 
                           const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
                           int* dev_status, int32_t* indptr, int32_t* indices, cudaStream_t st,
                           int* launches);
-struct AttnArgs {
-  const int32_t* page_table;
-  const int32_t* indptr;
-  const int32_t* indices;
-  void* out;
-  int out_f32;
-};
 cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 bool attn_2cta_supported(const Geo& g);
@@ -41,6 +34,8 @@ cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c,
 cudaError_t launch_gather_pages(const cpa_kv_cache& c, const int32_t* indptr, const int32_t* indices, const Geo& g,
                                 long long ps, long long hs, void* ck, void* cv, int32_t* cpt, cudaStream_t st,
                                 int* launches);
+cudaError_t launch_expand_tables(const int32_t* indptr, const int32_t* indices, const Geo& g, uint32_t* mask,
+                                 cudaStream_t st, int* launches);
 cudaError_t launch_row_max(const int* mstar_key, const Geo& g, float* row_max, cudaStream_t st,
                            int* launches);
 }  // namespace cpa
@@ -277,7 +272,7 @@ int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cp
 
 int attention_launch(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
                      int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
-                     const int32_t* indices, void* o, cudaStream_t st) {
+                     const int32_t* indices, void* o, cudaStream_t st, const uint32_t* mask = nullptr) {
   CUtensorMap tq, tk, tv;
   int s;
   if ((s = q_map(&tq, q, g)) != CPA_OK) return s;
@@ -287,10 +282,11 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
   a.page_table = page_table;
   a.indptr = indptr;
   a.indices = indices;
+  a.mask = mask;
   a.out = o;
   a.out_f32 = (p->flags & CPA_F_OUT_F32) ? 1 : 0;
   cudaError_t e;
-  if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA)) {
+  if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA) && mask == nullptr) {
     CUtensorMap tkh;  // half a page of keys per CTA of the pair
     if ((s = kv_map(&tkh, k_pages, g, num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
     e = launch_paged_attention_2cta(tq, tkh, tv, g, a, st, &g_launches);
@@ -442,6 +438,37 @@ int cpa_paged_attention_copy(const cpa_params* p, const void* q, const cpa_kv_ca
                               st)) != CPA_OK)
       return s;
   }
+  return CPA_OK;
+}
+
+int cpa_block_sparse_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache, const uint32_t* mask,
+                               void* o, void* ws, size_t ws_bytes, void* stream) {
+  (void)ws;
+  (void)ws_bytes;
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  if (!q || !o || !mask) return fail(CPA_ERR_NULL, "q/o/mask is NULL");
+  if (!aligned16(q) || !aligned16(o)) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
+  if (g.bs != 128) return fail(CPA_ERR_UNSUPPORTED, "block-sparse execution needs block_size 128");
+  if (g.nkvb > 4096) return fail(CPA_ERR_UNSUPPORTED, "block-sparse execution needs nkvb <= 4096");
+  return attention_launch(p, g, q, cache->k_pages, cache->v_pages, cache->num_pages, ps, hs, cache->page_table,
+                          nullptr, nullptr, o, (cudaStream_t)stream, mask);
+}
+
+int cpa_expand_tables(const cpa_params* p, const cpa_tables* t, uint32_t* mask, void* stream) {
+  g_launches = 0;
+  Geo g;
+  int s, sms;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  if (!t || !t->kv_indptr || !t->kv_indices || !mask) return fail(CPA_ERR_NULL, "tables/mask is NULL");
+  cudaError_t e = launch_expand_tables(t->kv_indptr, t->kv_indices, g, mask, (cudaStream_t)stream, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "expand_tables");
   return CPA_OK;
 }
 

@@ -46,16 +46,9 @@ struct AttnCfg {
   static constexpr int kThreads = (kSoftmaxWarps + kConvWarps + 2) * 32;
   static constexpr int kTmemCols = NT == 2 ? 512 : 256;
   static constexpr int kOCol0 = NT * 128;          // O_t at kOCol0 + t*128; S_t^b at t*128 + b*64
-  static constexpr int kSmem = NT * kQBytes + (kKStages + kVStages) * kKVBytes + 1024 + 512;
+  static constexpr int kMaxList = NT == 1 ? 4096 : 0;  // block-sparse mode: the CTA's block list
+  static constexpr int kSmem = NT * kQBytes + (kKStages + kVStages) * kKVBytes + 1024 + 512 + 4 * kMaxList;
   static_assert(kSmem <= 232448, "shared memory budget");
-};
-
-struct AttnArgs {
-  const int32_t* page_table;
-  const int32_t* indptr;   // nullptr => dense (all blocks)
-  const int32_t* indices;
-  void* out;
-  int out_f32;
 };
 
 template <int D, int BS, int NT, bool PF16>
@@ -83,6 +76,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
   int* n_blocks_s = reinterpret_cast<int*>(tmem_slot + 1);
   int* row_start_s = n_blocks_s + 1;
+  int* blist = row_start_s + 1;  // [Cfg::kMaxList]
 
   // ---- tile coordinates (heaviest q-tiles first)
   const int HP = g.E / NT;                     // head groups of NT per execution group
@@ -140,6 +134,42 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     *n_blocks_s = n;
     *row_start_s = start;
   }
+  if constexpr (Cfg::kMaxList > 0) {
+    // block-sparse execution: this CTA's tile (b, h0, q-block qt) runs
+    // the blocks set in its own 2D mask row, interpreted here: warp-wide popc + exclusive scan of the
+    // row's words (bits j <= jmax only), ascending block ids into shared memory.
+    if (warp == kTmaWarp && args.mask != nullptr) {
+      const int jmax = (g.P + min(p0 + 127, g.C - 1)) / g.bs;
+      const int wmax = jmax >> 5;
+      const uint32_t* mrow = args.mask + ((long long)(b * g.Hq + h0) * g.nqb + qt) * g.nwords;
+      int base = 0;
+      for (int w0 = 0; w0 <= wmax; w0 += 32) {
+        const int w = w0 + (int)lane;
+        uint32_t bits = 0;
+        if (w <= wmax) {
+          bits = __ldg(mrow + w);
+          if (w == wmax && (jmax & 31) != 31) bits &= (2u << (jmax & 31)) - 1u;
+        }
+        const int c = __popc(bits);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if ((int)lane >= o) incl += y;
+        }
+        int pos = base + incl - c;
+        while (bits) {
+          blist[pos++] = w * 32 + __ffs(bits) - 1;
+          bits &= bits - 1u;
+        }
+        base += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) {
+        *n_blocks_s = base;
+        *row_start_s = 0;
+      }
+    }
+  }
   if (warp == kMmaWarp) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -148,6 +178,12 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
   const int N = *n_blocks_s;          // pages
   const int U = N * SPB;              // sub-blocks
   const int row_start = *row_start_s;
+  // logical KV block of the CTA's n-th list entry
+  auto block_of = [&](int n) -> int {
+    if constexpr (Cfg::kMaxList > 0)
+      if (args.mask != nullptr) return blist[n];
+    return args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
+  };
 
   // TMA and MMA roles run on all 32 lanes with warp-uniform control flow (so descriptors and
   // coordinates live in uniform registers); one elected lane issues each TMA / tcgen05 instruction.
@@ -164,7 +200,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
       __syncwarp();
       const int32_t* ptab = args.page_table + (long long)b * g.maxb;
       for (int n = 0; n < N; ++n) {
-        const int j = args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
+        const int j = block_of(n);
         const int page = __ldg(ptab + j);
         const int ks = n % Cfg::kKStages, vs = n % Cfg::kVStages;
         mbar_wait(k_empty + ks, ((n / Cfg::kKStages) & 1) ^ 1);
@@ -309,7 +345,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
     int j = 0;
     for (int u = 0; u < U; ++u) {
-      if (u % SPB == 0) j = args.indptr != nullptr ? __ldg(args.indices + row_start + u / SPB) : u / SPB;
+      if (u % SPB == 0) j = block_of(u / SPB);
       const uint32_t s_tm = tmem + lane_off + t * 128 + (u & 1) * 64;
       if (row == 0) TRACE(4, 2 * u + t);
       mbar_wait(s_full + 2 * t + (u & 1), (u >> 1) & 1);
@@ -457,7 +493,7 @@ static cudaError_t launch_attn_t(const CUtensorMap& tq, const CUtensorMap& tk, c
 cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches) {
   ++*launches;
-  const bool pair = (g.E % 2) == 0;
+  const bool pair = (g.E % 2) == 0 && a.mask == nullptr;  // block-sparse: one head per CTA
 #define CPA_AT(DD, BB)                                                        \
   if (g.d == DD && g.bs == BB) {                                              \
     if (g.flags & (1u << 8))                                                  \

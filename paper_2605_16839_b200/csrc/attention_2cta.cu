@@ -42,14 +42,6 @@ struct Attn2Cfg {
   static_assert(kSmem <= 232448, "shared memory budget");
 };
 
-struct AttnArgs {
-  const int32_t* page_table;
-  const int32_t* indptr;   // nullptr => dense (all blocks)
-  const int32_t* indices;
-  void* out;
-  int out_f32;
-};
-
 template <int BS, bool PF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     k_paged_attn_2cta(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k_half,

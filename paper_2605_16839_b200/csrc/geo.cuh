@@ -22,4 +22,18 @@ __host__ __device__ inline int group_kv_head(const Geo& g, int grp) {
   return (grp * g.E) / g.kv_per_q;
 }
 
+// Arguments of the paged-attention kernels. Block list of a CTA, in priority order:
+//   mask    != nullptr: the set bits of its per-(b, h, q-block) 2D mask row (block-sparse execution,
+//                       1-CTA kernel only; mask layout [B, Hq, nqb, nwords] u32, LSB-first);
+//   indptr  != nullptr: its CSR table row b*Gn + g (zero-copy paged execution);
+//   else               every block (dense baseline).
+struct AttnArgs {
+  const int32_t* page_table;
+  const int32_t* indptr;
+  const int32_t* indices;
+  const uint32_t* mask;
+  void* out;
+  int out_f32;
+};
+
 }  // namespace cpa

@@ -138,4 +138,35 @@ cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& 
   return cudaGetLastError();
 }
 
+// Fig. 7(c) ablation ("the same unioned block mask"; SPEC.md:447 q-uniform expansion):
+// Mq[b,h,i,j] = [j in T[b, h/E]] && j <= jmax(i), the table row of h's execution group repeated over
+// every q-block i and cut to the causal-valid tiles. One CTA per (q-block i, b*Hq + h), word-wise
+// OR in shared memory.
+__global__ void __launch_bounds__(128)
+    k_expand_tables(const int32_t* __restrict__ indptr, const int32_t* __restrict__ indices, Geo g,
+                    uint32_t* __restrict__ mask) {
+  extern __shared__ uint32_t words[];
+  const int i = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / g.Hq, h = bh % g.Hq;
+  const int r = b * g.Gn + h / g.E;
+  const int jmax = (g.P + min((i + 1) * g.bs, g.C) - 1) / g.bs;
+  for (int w = threadIdx.x; w < g.nwords; w += blockDim.x) words[w] = 0u;
+  __syncthreads();
+  const int end = indptr[r + 1];
+  for (int k = indptr[r] + threadIdx.x; k < end; k += blockDim.x) {
+    const int j = indices[k];
+    if (j <= jmax) atomicOr(&words[j >> 5], 1u << (j & 31));
+  }
+  __syncthreads();
+  uint32_t* dst = mask + ((long long)bh * g.nqb + i) * g.nwords;
+  for (int w = threadIdx.x; w < g.nwords; w += blockDim.x) dst[w] = words[w];
+}
+
+cudaError_t launch_expand_tables(const int32_t* indptr, const int32_t* indices, const Geo& g, uint32_t* mask,
+                                 cudaStream_t st, int* launches) {
+  k_expand_tables<<<dim3(g.nqb, g.B * g.Hq), 128, g.nwords * 4, st>>>(indptr, indices, g, mask);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
 }  // namespace cpa
