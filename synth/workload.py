@@ -122,8 +122,12 @@ def _betas(d: int):
 
 
 def make_kv(cfg: Config, seed: int, rho: float = 0.30, length: Optional[int] = None,
-            kv_heads: Optional[range] = None, needles: bool = True):
-    """Logical flat K, V [B, Hkv_sel, L, d] float32 (bf16-valued)."""
+            kv_heads: Optional[range] = None, needles: bool = True, graded: bool = False):
+    """Logical flat K, V [B, Hkv_sel, L, d] float32 (bf16-valued).
+
+    graded=True (alpha-sweep workload): needle j's key boost is scaled by
+    its own gain ~ U(0.1, 1), so the needles' pooled-logit gaps spread over ~0.6..6 nats and the
+    threshold alpha decides how many of them are kept."""
     L = cfg.context if length is None else length
     d = cfg.head_dim
     heads = range(cfg.num_kv_heads) if kv_heads is None else kv_heads
@@ -139,11 +143,13 @@ def make_kv(cfg: Config, seed: int, rho: float = 0.30, length: Optional[int] = N
                 U = _topics(seed, b, g, d, n_topics(cfg))
                 kk -= (kk @ U) @ U.T
                 blocks, topics = needle_plan(cfg, seed, rho, b, g)
+                gains = (_key(seed, "grade", b, g).uniform(0.1, 1.0, size=len(blocks)) if graded
+                         else np.ones(len(blocks)))
                 bs = cfg.block_size
-                for j, c in zip(blocks, topics):
+                for j, c, gn in zip(blocks, topics, gains):
                     lo, hi_ = j * bs, min((j + 1) * bs, L)
                     if lo < L:
-                        kk[lo:hi_] += beta_k * U[:, c]
+                        kk[lo:hi_] += (gn * beta_k) * U[:, c]
             k[b, hi] = round_bf16(kk)
             v[b, hi] = round_bf16(vv)
     return k, v
