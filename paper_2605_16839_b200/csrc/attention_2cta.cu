@@ -61,8 +61,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* v_empty = v_full + Cfg::kVStages;       // both: V stage consumed (multicast commit)
   uint64_t* v_ready = v_empty + Cfg::kVStages;      // leader: both V halves converted (4 arrivals)
   uint64_t* s_full = v_ready + Cfg::kVStages;       // both [2]: S^b computed (multicast commit)
-  uint64_t* p_full = s_full + 2;                    // leader [2]: P^b written by both softmax WGs
-  uint64_t* pv_done = p_full + 2;                   // both [2]: last P.V into O_b complete
+  uint64_t* p_full = s_full + 2;                    // leader [2][2]: P^b columns of WG w written
+  uint64_t* pv_done = p_full + 4;                   // both [2]: last P.V into O_w complete
   uint64_t* o_full = pv_done + 2;                   // both: every MMA complete
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
   int* n_blocks_s = reinterpret_cast<int*>(tmem_slot + 1);
@@ -101,8 +101,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(s_full + 1, 1);
-    mbar_init(p_full, 8);  // 4 softmax warps of WG b x 2 CTAs
-    mbar_init(p_full + 1, 8);
+    for (int i = 0; i < 4; ++i) mbar_init(p_full + i, 8);  // 4 softmax warps of WG w x 2 CTAs
     mbar_init(pv_done, 1);
     mbar_init(pv_done + 1, 1);
     mbar_init(o_full, 1);
@@ -195,18 +194,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
         __syncwarp();
       };
-      auto issue_pv = [&](int n) {  // O_b += P^b V_n (b = n%2), M=256, N=d (64 cols per CTA), K=BS
-        const uint32_t p_tm = tmem + (n & 1) * 128;
-        const uint32_t o_tm = tmem + 256 + (n & 1) * 128;
-        const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kVHalf;
+      // O_w += P_w V_n[w-half keys]: WG w's P (keys [w BS/2, (w+1) BS/2) of page n, fp16 packed over its
+      // S^b columns) times those V rows; M=256, N=d (64 cols per CTA), K=BS/2
+      auto issue_pv = [&](int n, int w) {
+        const uint32_t p_tm = tmem + (n & 1) * 128 + w * (BS / 2);
+        const uint32_t o_tm = tmem + 256 + w * 128;
+        const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kVHalf + w * (BS / 2) * 128;
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BS / 16; ++kk) {
+          for (int kk = 0; kk < BS / 32; ++kk) {
             const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
-            mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (n > 1 || kk > 0) ? 1u : 0u);
+            mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (n > 0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit2(pv_done + (n & 1));
-          tc_commit2(v_empty + n % Cfg::kVStages);
+          tc_commit2(pv_done + w);
+          if (w == 1) tc_commit2(v_empty + n % Cfg::kVStages);
         }
         __syncwarp();
       };
@@ -223,10 +224,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int n = 0; n < N; ++n) {
         mbar_wait(v_ready + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
         if (lane == 0) TRACE2(1, n);
-        mbar_wait(p_full + (n & 1), (n >> 1) & 1);
+        mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
         if (lane == 0) TRACE2(2, n);
         tc_fence_after();
-        issue_pv(n);
+        issue_pv(n, 0);
+        mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+        tc_fence_after();
+        issue_pv(n, 1);
         if (lane == 0) TRACE2(9, n);
         if (n + 2 < N) {
           wait_k(n + 2);
@@ -277,31 +281,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const int lim = min(g.P + p, g.L - 1);
     const float sl2 = g.scale * 1.4426950408889634f;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t s_tm = tmem + lane_off + wg * 128;        // S^wg (this row's lanes)
+    constexpr int HC = BS / 2;                                // key columns of a page per WG
+    const uint32_t s_tm0 = tmem + lane_off + wg * HC;         // WG's columns of S^0 (this row's lanes)
     const uint32_t o_tm = tmem + lane_off + 256 + wg * 128;  // O_wg
     float m_run = -INFINITY, l_run = 0.f;
-    for (int n = wg; n < N; n += 2) {
-      const int use = n >> 1;  // how many pages this WG has processed before
+    // Both WGs work on every page: WG w owns key columns [w BS/2, (w+1) BS/2) of each S^b with its own
+    // running max / sum and its own accumulator O_w (no cross-WG exchange until the epilogue merge).
+    for (int n = 0; n < N; ++n) {
+      const uint32_t s_tm = s_tm0 + (n & 1) * 128;
       if (row == 0) TRACE2(4 + 16 * wg, n);
-      mbar_wait(s_full + wg, use & 1);
+      mbar_wait(s_full + (n & 1), (n >> 1) & 1);
       if (row == 0) TRACE2(5 + 16 * wg, n);
       tc_fence_after();
-      uint32_t sv[BS / 32][32];
+      uint32_t sv[HC / 32][32];
 #pragma unroll
-      for (int k = 0; k < BS / 32; ++k) tmem_ld32(s_tm + k * 32, sv[k]);
+      for (int k = 0; k < HC / 32; ++k) tmem_ld32(s_tm + k * 32, sv[k]);
       tmem_wait_ld();
       if (n >= n_diag) {  // block crosses the causal diagonal of this tile: mask in absolute positions
         const int j = args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
-        const int tbase = j * g.bs;
+        const int tbase = j * g.bs + wg * HC;
 #pragma unroll
-        for (int k = 0; k < BS / 32; ++k)
+        for (int k = 0; k < HC / 32; ++k)
 #pragma unroll
           for (int c = 0; c < 32; ++c)
             if (tbase + k * 32 + c > lim) sv[k][c] = __float_as_uint(-INFINITY);
       }
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int k = 0; k < BS / 32; ++k)
+      for (int k = 0; k < HC / 32; ++k)
 #pragma unroll
         for (int c = 0; c < 32; c += 8)
 #pragma unroll
@@ -320,7 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       // polynomial (FMA pipe), the rest on MUFU.EX2; 4 partial f32x2 sums; fp16 pack; stored over S.
       float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
-      for (int k = 0; k < BS / 32; ++k) {
+      for (int k = 0; k < HC / 32; ++k) {
         uint32_t pk[16];
 #pragma unroll
         for (int q2 = 0; q2 < 16; ++q2) {
@@ -340,9 +347,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
       l_run = l_run * f + ((a01.x + a01.y) + (a23.x + a23.y));
       if (row == 0) TRACE2(12 + 16 * wg, n);
-      // rescale O_wg (own rows) after this WG's previous P.V completed, before PV(n) is issued
-      if (__any_sync(0xffffffffu, rescale && use > 0)) {
-        mbar_wait(pv_done + wg, (use - 1) & 1);
+      // rescale O_wg (own rows) after this WG's previous P.V completed, before PV_wg(n) is issued
+      if (__any_sync(0xffffffffu, rescale && n > 0)) {
+        mbar_wait(pv_done + wg, (n - 1) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
@@ -358,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full + wg, 0);
+      if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
       if (row == 0) TRACE2(6 + 16 * wg, n);
     }
     // ---- epilogue: merge the two half-softmaxes, O = (O_0 a_0 + O_1 a_1) / (l_0 a_0 + l_1 a_1),
@@ -372,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const float lt = l0 * a0 + l1 * a1;
     const float inv = lt > 0.f ? 1.0f / lt : 0.f;
     const float c0f = a0 * inv, c1f = a1 * inv;
-    const bool has0 = N > 0, has1 = N > 1;  // O_1 is only written when there are >= 2 pages
+    const bool has0 = N > 0, has1 = N > 0;  // both accumulators are written on every page
     const bool store = p < g.C;
     if (N > 0) {
       mbar_wait(o_full, 0);

@@ -32,3 +32,11 @@ for n in list(range(0, 4)) + list(range(N // 2, N // 2 + 4)):
         "wg": n % 2, "sm_wait": d(tr[5 + 16*(n%2), n], tr[4 + 16*(n%2), n]),
         "sm_ld_max": d(tr[11 + 16*(n%2), n], tr[5 + 16*(n%2), n]), "sm_exp": d(tr[12 + 16*(n%2), n], tr[11 + 16*(n%2), n]),
         "sm_tail": d(tr[6 + 16*(n%2), n], tr[12 + 16*(n%2), n]), "conv": d(tr[8, n], tr[7, n])}))
+# absolute timeline (cycles from the first listed event) of a few mid-kernel pages
+b0 = N // 2
+t0 = int(tr[5 + 16 * (b0 % 2), b0])
+for n in range(b0, b0 + 6):
+    w = n % 2
+    r = lambda e: int(tr[e, n]) - t0
+    print(f"page {n} wg{w}: s_ready {r(5 + 16*w):6d}  max_done {r(11 + 16*w):6d}  exp_done {r(12 + 16*w):6d}  "
+          f"p_arrive {r(6 + 16*w):6d} | mma: p_seen {r(2):6d} pv_issued {r(9):6d} s(n+2)_issued {r(3):6d}")
