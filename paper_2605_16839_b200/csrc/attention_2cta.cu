@@ -10,9 +10,9 @@
 // columns [64r, 64r+64) of V, so per SM the tensor core reads 6 KB of shared memory per 64-cycle
 // S MMA (96 B/clk, under the 128 B/clk limit that caps a 1-CTA 128x128 SS MMA) and the TMA / L2
 // traffic per FLOP halves. P (fp16) aliases S^b; the MMA computes S(n+1) while the softmax of S(n)
-// runs. Two softmax warpgroups run independent online softmaxes over alternate pages of the table
-// (WG b takes pages n = b mod 2 with S^b, P^b and its own accumulator O_b), so two softmax warps
-// share each SMSP out of phase; the epilogue merges (m_b, l_b, O_b) of the two halves.
+// runs. Both softmax warpgroups work on every page: WG w owns key columns [w BS/2, (w+1) BS/2) of
+// each S^b and keeps its own running max / sum and accumulator O_w (P.V of its half of the keys),
+// so the two WGs never exchange anything per page; the epilogue merges (m_w, l_w, O_w).
 // TMEM per CTA: S^0 [0,128) S^1 [128,256) O_0 [256,384) O_1 [384,512).
 // Warps: 0-7 softmax (WG = warp/4, lane quarter = warp%4), 8-9 V bf16->fp16 converters,
 // 10 TMA producer, 11 TMEM alloc + MMA issuer.
