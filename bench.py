@@ -10,7 +10,9 @@ paged attention over the tabled blocks, for the FINAL chunk of the workload (KV 
 Prints ONE JSON line (rank 0). value = attention ms per chunk (lower is better), inputs resident
 in HBM, L2 flushed before every timed step (a 512 MiB write), CUDA events on the launch stream,
 max over ranks. N > 1: KV-head groups are sharded over ranks (one KV group per GPU at N=8) and
-the per-rank head outputs are all-gathered over NCCL each step (strong scaling: one chunk).
+the per-rank head outputs are all-gathered each step (strong scaling: one chunk) -- by default
+inside the attention kernel (P2P stores into every rank's symmetric-memory buffer over NVLink + a
+signal barrier, cpa_chunk_step_peer); --collective nccl times NCCL all_gather_into_tensor instead.
 """
 from __future__ import annotations
 
@@ -169,6 +171,29 @@ def cpu_oracle_sample(cfg, seed, q, k, v, P, C, budget_s=15.0):
 
 
 # ------------------------------------------------------------------------------ GPU arm
+def peer_setup(torch, dist, cpa, full_shape, world, rank):
+    """Symmetric-memory gathered output [B, C, Hq, d] + uint32 signal pads [W] on every rank, mapped
+    into every peer (torch symmetric memory = CUDA IPC / fabric handles over NVLink)."""
+    import torch.distributed._symmetric_memory as symm
+    group = dist.group.WORLD
+    try:
+        symm.enable_symm_mem_for_group(group.group_name)
+    except Exception:  # noqa: BLE001 -- newer torch enables it implicitly
+        pass
+    buf = symm.empty(full_shape, dtype=torch.bfloat16, device="cuda")
+    hb = symm.rendezvous(buf, group)
+    sig = symm.empty(world, dtype=torch.int32, device="cuda")
+    sig.zero_()
+    hs = symm.rendezvous(sig, group)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    dist.barrier()
+    peers = cpa.PeerOut(world, rank, list(hb.buffer_ptrs), list(hs.buffer_ptrs), timeout_ms=20000,
+                        dev_status=status)
+    peers._keep = (buf, sig, hb, hs)
+    return peers, buf
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -185,7 +210,10 @@ def run_gpu(args):
         local = 0
     torch.cuda.set_device(local)
     backend = "gloo" if one_dev else "nccl"
-    if world > 1:
+    # CPA_BENCH_PEER_W1=1 (test only, under torchrun --nproc-per-node 1): a 1-rank NCCL group so the
+    # fused peer path runs through real symmetric memory on a single-GPU box.
+    force_peer = os.environ.get("CPA_BENCH_PEER_W1") == "1" and world == 1
+    if world > 1 or force_peer:
         if one_dev:
             dist.init_process_group("gloo")
         else:
@@ -223,8 +251,24 @@ def run_gpu(args):
     o_all = torch.empty(world, cfg.batch, C, hq_l, d, dtype=torch.bfloat16, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    # N > 1: the head-output all-gather is fused into the attention epilogue (P2P stores into every
+    # rank's symmetric-memory buffer + a signal barrier, cpa_chunk_step_peer); NCCL all-gather after a
+    # local step is the baseline (--collective nccl) and the fallback if symmetric memory is unavailable.
+    collective = "none" if world == 1 and not force_peer else ("gloo all-gather" if one_dev else args.collective)
+    peers = None
+    if collective == "peer":
+        try:
+            peers, o_gathered = peer_setup(torch, dist, cpa, (cfg.batch, C, cfg.num_q_heads, d), world, rank)
+            collective = "fused peer-store all-gather (NVLink P2P, cpa_chunk_step_peer)"
+        except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+            collective = f"nccl all-gather (symmetric memory unavailable: {type(ex).__name__}: {ex})"[:200]
+    elif collective == "nccl":
+        collective = "nccl all-gather"
 
     def step():
+        if peers is not None:
+            cpa.chunk_step_peer(p, dq, cache, tables, peers, kc, vc, workspace=ws)
+            return
         cpa.chunk_step(p, dq, cache, tables, o, kc, vc, workspace=ws)
         if world > 1:
             allgather_heads(o, o_all)
@@ -257,6 +301,8 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
     ms = max_over_ranks([float(np.mean(ts))])[0]
+    if peers is not None and int(peers.dev_status.item()) != 0:
+        raise RuntimeError(f"rank {rank}: peer barrier timed out waiting for rank {int(peers.dev_status.item()) - 1}")
 
     # ---- stage breakdown and the dense baseline (same kernels, tables = all blocks)
     reps = max(3, min(args.steps, 10))
@@ -290,6 +336,10 @@ def run_gpu(args):
         dq2.copy_(hq_pin, non_blocking=True)
         kc2.copy_(hk_pin, non_blocking=True)
         vc2.copy_(hv_pin, non_blocking=True)
+        if peers is not None:
+            cpa.chunk_step_peer(p, dq2, cache, tables, peers, kc2, vc2, workspace=ws)
+            ho_pin.copy_(o_gathered[:, :, rank * hq_l:(rank + 1) * hq_l], non_blocking=True)
+            return
         cpa.chunk_step(p, dq2, cache, tables, o, kc2, vc2, workspace=ws)
         if world > 1:
             allgather_heads(o, o_all)
@@ -321,7 +371,7 @@ def run_gpu(args):
                        "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": d,
                        "block_size": bs, "alpha": ALPHA, "needle_density": RHO, "exec_group_size": E_exec,
                        "scorer": "exact tile max (SPEC.md:223)" if args.exact_scores else "pooled query (SPEC.md:269)",
-                       "parallelism": f"kv-group shard x{world}" + (f" + {backend} all-gather" if world > 1 else ""),
+                       "parallelism": f"kv-group shard x{world}" + (f" + {collective}" if collective != "none" else ""),
                        "l2": "flushed (512 MiB write) before every timed step"},
             "dense_ms_per_chunk": round(t_dense, 4),
             "speedup_vs_dense": round(t_dense / ms, 3),
@@ -342,7 +392,7 @@ def run_gpu(args):
             "paper_context": "2.72x attention speedup at 128K on 2xH200 (TP=2, B=8, chunk 1024; PAPER.md:612, 620)",
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
         dist.destroy_process_group()
 
@@ -387,6 +437,8 @@ def main():
     ap.add_argument("--exec-group", type=int, default=0,
                     help="execution-group size E (0 = full KV group; 4 = sub-KV-group union, PAPER.md:498)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
+                    help="N>1 head-output all-gather: fused P2P stores in the attention epilogue, or NCCL")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -166,6 +166,52 @@ CPA_API int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chu
 CPA_API int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk,
                   const cpa_kv_cache* cache, void* stream);
 
+/* ---- Multi-GPU: head-group sharding with the output all-gather fused into the attention epilogue.
+ * The chunk step shards by execution group with no data-path exchange: every table is per (b, g)
+ * (PAPER.md:203-209), so rank r of W owns KV heads [r*Hkv/W, (r+1)*Hkv/W) and their query heads (the
+ * attention half of the paper's tensor-parallel setting). The only exchange is the
+ * all-gather of the head outputs, which cpa_chunk_step_peer performs inside the attention kernel: each
+ * normalised O tile is stored to every rank's gathered buffer through NVLink peer mappings (P2P stores),
+ * then a one-warp barrier signals every peer and waits for every peer's signal.
+ *
+ * Buffers (all DEVICE pointers mapped into the calling process, e.g. CUDA IPC / torch symmetric
+ * memory; none is allocated or retained by libcpa):
+ *   peer_out[w]:    rank w's gathered output [B, C, W*Hq, d] (Hq = this call's p->num_q_heads, the same
+ *                   on every rank), bf16 (fp32 with CPA_F_OUT_F32), token stride out_token_stride
+ *                   (0 => W*Hq*d elements). Rank r writes heads [r*Hq, (r+1)*Hq) of every peer_out[w].
+ *   peer_signal[w]: rank w's signal pad, uint32 [W], zero-initialised once before the first call.
+ *                   Slot w' of rank w's pad is written only by rank w'.
+ * epoch: strictly increasing across calls on the same pads (1, 2, 3, ...); the call returns (stream
+ *   order) after every rank has posted `epoch`, i.e. after every peer_out[rank] is complete.
+ * Reuse: a rank must not read its peer_out buffer for call k+1's purposes before that call's barrier,
+ *   and must have finished reading call k's contents before ANY rank starts call k+1 (alternate two
+ *   buffer sets, or call cpa_peer_barrier with a fresh epoch first).
+ * dev_status (optional int32[1]): set to 1 + w if peer w did not post within timeout_ms (0 => 10000);
+ *   the barrier then stops waiting instead of hanging the GPU. */
+#define CPA_MAX_PEERS 8
+typedef struct {
+  int32_t world;                  /* W in [1, CPA_MAX_PEERS] */
+  int32_t rank;                   /* r in [0, W) */
+  void* const* peer_out;          /* HOST array [W] of device pointers (see above) */
+  int64_t out_token_stride;       /* elements; 0 => W*Hq*d */
+  uint32_t* const* peer_signal;   /* HOST array [W] of device pointers */
+  uint32_t epoch;                 /* >= 1 */
+  uint32_t timeout_ms;            /* 0 => 10000 */
+  int32_t* dev_status;            /* optional */
+} cpa_peer_out;
+
+/* cpa_chunk_step with the head-output all-gather fused in (see above): optional append, tables,
+ * attention whose epilogue writes every peer_out[w] at this rank's head slice, then the barrier.
+ * p describes this rank's shard (Hq, Hkv = its own heads); q / k_chunk / v_chunk / cache / tables as in
+ * cpa_chunk_step. Errors: CPA_ERR_NULL (missing peer arrays/pointers), CPA_ERR_SHAPE (W or rank out of
+ * range, out_token_stride < W*Hq*d), CPA_ERR_MISALIGNED (a peer pointer not 16B aligned). */
+CPA_API int cpa_chunk_step_peer(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                                const cpa_kv_cache* cache, cpa_tables* tables, const cpa_peer_out* peers,
+                                void* ws, size_t ws_bytes, void* stream);
+
+/* The barrier alone (signal every peer with `epoch`, wait for all); peer_out is not used. */
+CPA_API int cpa_peer_barrier(const cpa_peer_out* peers, void* stream);
+
 /* NEXT-3 execution ablation only ("CompactAttention-FP (Copy)"): gather the
  * tabled K/V pages of every (b, g) row into a compact pool in `ws` (an explicit KV copy, exactly what
  * the zero-copy path avoids), then run the same attention kernel over the compact pool through a

@@ -17,7 +17,8 @@ import torch
 __all__ = [
     "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
     "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
-    "paged_attention_copy", "block_sparse_attention", "expand_tables",
+    "paged_attention_copy", "block_sparse_attention", "expand_tables", "PeerOut", "chunk_step_peer",
+    "peer_barrier",
     "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "EXPORTED_SYMBOLS",
 ]
 
@@ -29,7 +30,8 @@ STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA
           "CPA_ERR_ALPHA", "CPA_ERR_WORKSPACE", "CPA_ERR_CAPACITY", "CPA_ERR_CUDA"]
 EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",
                     "cpa_append_kv", "cpa_copy_workspace_bytes", "cpa_paged_attention_copy",
-                    "cpa_block_sparse_attention", "cpa_expand_tables", "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
+                    "cpa_block_sparse_attention", "cpa_expand_tables", "cpa_chunk_step_peer",
+                    "cpa_peer_barrier", "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
 
 
 class CpaError(RuntimeError):
@@ -56,6 +58,12 @@ class _Tables(ctypes.Structure):
     _fields_ = [("kv_indptr", ctypes.c_void_p), ("kv_indices", ctypes.c_void_p), ("capacity", ctypes.c_int64),
                 ("mask_bits", ctypes.c_void_p), ("scores", ctypes.c_void_p), ("row_max", ctypes.c_void_p),
                 ("dev_status", ctypes.c_void_p)]
+
+
+class _PeerOut(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("rank", ctypes.c_int32), ("peer_out", ctypes.POINTER(ctypes.c_void_p)),
+                ("out_token_stride", ctypes.c_int64), ("peer_signal", ctypes.POINTER(ctypes.c_void_p)),
+                ("epoch", ctypes.c_uint32), ("timeout_ms", ctypes.c_uint32), ("dev_status", ctypes.c_void_p)]
 
 
 _lib = None
@@ -88,7 +96,11 @@ def lib() -> ctypes.CDLL:
         L.cpa_block_sparse_attention.restype = i32
         L.cpa_expand_tables.argtypes = [ctypes.POINTER(Params), ctypes.POINTER(_Tables), vp, vp]
         L.cpa_expand_tables.restype = i32
-        for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv):
+        L.cpa_chunk_step_peer.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(_Cache),
+                                          ctypes.POINTER(_Tables), ctypes.POINTER(_PeerOut), vp, ctypes.c_size_t, vp]
+        L.cpa_peer_barrier.argtypes = [ctypes.POINTER(_PeerOut), vp]
+        for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv,
+                  L.cpa_chunk_step_peer, L.cpa_peer_barrier):
             f.restype = i32
         L.cpa_status_string.argtypes = [i32]
         L.cpa_status_string.restype = ctypes.c_char_p
@@ -184,16 +196,18 @@ def alloc_tables(p: Params, device="cuda", mask: bool = False, scores: bool = Fa
     return t
 
 
-def _ws(p: Params, workspace: Optional[torch.Tensor], device) -> torch.Tensor:
+def _ws(p: Params, workspace: Optional[torch.Tensor], device, stream=None) -> torch.Tensor:
     need = workspace_bytes(p)
     if workspace is None:
         workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=device)
+        if isinstance(stream, torch.cuda.Stream):  # freed on return: keep it until `stream` is done with it
+            workspace.record_stream(stream)
     return workspace
 
 
 def build_tables(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables,
                  workspace: Optional[torch.Tensor] = None, stream=None) -> BlockTables:
-    ws = _ws(p, workspace, q.device if q is not None else cache.k_pages.device)
+    ws = _ws(p, workspace, q.device if q is not None else cache.k_pages.device, stream)
     c, t = cache._c(), tables._c()
     _check(lib().cpa_build_tables(ctypes.byref(p), _ptr(q), ctypes.byref(c), ctypes.byref(t),
                                   _ptr(ws), ws.numel(), _stream(stream)))
@@ -202,7 +216,7 @@ def build_tables(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockT
 
 def paged_attention(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: Optional[BlockTables],
                     out: torch.Tensor, workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    ws = _ws(p, workspace, q.device)
+    ws = _ws(p, workspace, q.device, stream)
     c = cache._c()
     t = tables._c() if tables is not None else None
     _check(lib().cpa_paged_attention(ctypes.byref(p), _ptr(q), ctypes.byref(c),
@@ -214,11 +228,46 @@ def paged_attention(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: Opt
 def chunk_step(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables, out: torch.Tensor,
                k_chunk: Optional[torch.Tensor] = None, v_chunk: Optional[torch.Tensor] = None,
                workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-    ws = _ws(p, workspace, q.device)
+    ws = _ws(p, workspace, q.device, stream)
     c, t = cache._c(), tables._c()
     _check(lib().cpa_chunk_step(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
                                 ctypes.byref(t), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
     return out
+
+
+class PeerOut:
+    """Peer mappings for cpa_chunk_step_peer (see cpa.h): W gathered output buffers [B, C, W*Hq, d]
+    and W uint32 signal pads, given as raw device addresses valid in this process (torch symmetric
+    memory buffer_ptrs, CUDA IPC, or -- in single-GPU tests -- plain tensors on one device). The
+    epoch advances by one per call."""
+
+    def __init__(self, world: int, rank: int, out_ptrs, signal_ptrs, out_token_stride: int = 0,
+                 timeout_ms: int = 0, dev_status: Optional[torch.Tensor] = None):
+        assert len(out_ptrs) == world and len(signal_ptrs) == world
+        self._outs = (ctypes.c_void_p * world)(*[int(x) for x in out_ptrs])
+        self._sigs = (ctypes.c_void_p * world)(*[int(x) for x in signal_ptrs])
+        self.world, self.rank, self.epoch = world, rank, 0
+        self.out_token_stride, self.timeout_ms, self.dev_status = out_token_stride, timeout_ms, dev_status
+
+    def _next(self) -> _PeerOut:
+        self.epoch += 1
+        return _PeerOut(self.world, self.rank, self._outs, self.out_token_stride, self._sigs, self.epoch,
+                        self.timeout_ms, _ptr(self.dev_status))
+
+
+def chunk_step_peer(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables, peers: PeerOut,
+                    k_chunk: Optional[torch.Tensor] = None, v_chunk: Optional[torch.Tensor] = None,
+                    workspace: Optional[torch.Tensor] = None, stream=None) -> None:
+    """cpa_chunk_step with the head-output all-gather fused into the attention epilogue (cpa.h)."""
+    ws = _ws(p, workspace, q.device, stream)
+    c, t, pr = cache._c(), tables._c(), peers._next()
+    _check(lib().cpa_chunk_step_peer(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
+                                     ctypes.byref(t), ctypes.byref(pr), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def peer_barrier(peers: PeerOut, stream=None) -> None:
+    pr = peers._next()
+    _check(lib().cpa_peer_barrier(ctypes.byref(pr), _stream(stream)))
 
 
 def append_kv(p: Params, k_chunk: torch.Tensor, v_chunk: torch.Tensor, cache: PagedKVCache, stream=None):

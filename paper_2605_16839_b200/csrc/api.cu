@@ -38,6 +38,7 @@ cudaError_t launch_expand_tables(const int32_t* indptr, const int32_t* indices, 
                                  cudaStream_t st, int* launches);
 cudaError_t launch_row_max(const int* mstar_key, const Geo& g, float* row_max, cudaStream_t st,
                            int* launches);
+cudaError_t launch_peer_barrier(const PeerSig& s, cudaStream_t st, int* launches);
 }  // namespace cpa
 
 using namespace cpa;
@@ -270,9 +271,18 @@ int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cp
   return CPA_OK;
 }
 
+// Output destinations of the attention epilogue (AttnArgs.outs): the call's own o, or the W gathered
+// buffers of a peer exchange (cpa_chunk_step_peer).
+struct OutSpec {
+  int n;
+  void* outs[kMaxOut];
+  long long stride, bstride;  // elements between tokens / batch entries
+};
+
 int attention_launch(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
                      int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
-                     const int32_t* indices, void* o, cudaStream_t st, const uint32_t* mask = nullptr) {
+                     const int32_t* indices, void* o, cudaStream_t st, const uint32_t* mask = nullptr,
+                     const OutSpec* os = nullptr) {
   CUtensorMap tq, tk, tv;
   int s;
   if ((s = q_map(&tq, q, g)) != CPA_OK) return s;
@@ -283,8 +293,19 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
   a.indptr = indptr;
   a.indices = indices;
   a.mask = mask;
-  a.out = o;
   a.out_f32 = (p->flags & CPA_F_OUT_F32) ? 1 : 0;
+  for (int k = 0; k < kMaxOut; ++k) a.outs[k] = nullptr;
+  if (os) {
+    a.n_out = os->n;
+    for (int k = 0; k < os->n; ++k) a.outs[k] = os->outs[k];
+    a.o_stride = os->stride;
+    a.o_bstride = os->bstride;
+  } else {
+    a.n_out = 1;
+    a.outs[0] = o;
+    a.o_stride = g.q_stride;
+    a.o_bstride = g.b_stride;
+  }
   cudaError_t e;
   if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA) && mask == nullptr) {
     CUtensorMap tkh;  // half a page of keys per CTA of the pair
@@ -298,12 +319,66 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
 }
 
 int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
-                   long long hs, const cpa_tables* t, void* o, cudaStream_t st) {
-  if (!q || !o) return fail(CPA_ERR_NULL, "q/o is NULL");
-  if (!aligned16(q) || !aligned16(o)) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
+                   long long hs, const cpa_tables* t, void* o, cudaStream_t st, const OutSpec* os = nullptr) {
+  if (!q || (!o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
+  if (!aligned16(q) || (!os && !aligned16(o))) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
   if (t && (!t->kv_indptr || !t->kv_indices)) return fail(CPA_ERR_NULL, "tables pointers");
   return attention_launch(p, g, q, c->k_pages, c->v_pages, c->num_pages, ps, hs, c->page_table,
-                          t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, st);
+                          t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, st, nullptr, os);
+}
+
+// append (optional) -> estimator + tables -> attention, the body of cpa_chunk_step(_peer)
+int chunk_step_impl(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                    const cpa_kv_cache* cache, cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
+                    cudaStream_t st, const OutSpec* os) {
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  if ((k_chunk == nullptr) != (v_chunk == nullptr)) return fail(CPA_ERR_NULL, "k_chunk/v_chunk: both or neither");
+  if (!q || (!o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
+  if (!tables) return fail(CPA_ERR_NULL, "tables is NULL");
+  int total = 0;
+  if (k_chunk) {
+    if (!aligned16(k_chunk) || !aligned16(v_chunk)) return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
+    cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, st, &g_launches);
+    if (e != cudaSuccess) return cuda_fail(e, "append");
+  }
+  total += g_launches;
+  g_launches = 0;
+  if ((s = build_tables_impl(p, g, q, cache, ps, hs, tables, ws, ws_bytes, st, sms)) != CPA_OK) return s;
+  total += g_launches;
+  g_launches = 0;
+  if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, st, os)) != CPA_OK) return s;
+  g_launches += total;
+  return CPA_OK;
+}
+
+int check_peers(const cpa_peer_out* pr) {
+  if (!pr || !pr->peer_signal) return fail(CPA_ERR_NULL, "peers / peer_signal is NULL");
+  if (pr->world < 1 || pr->world > CPA_MAX_PEERS || pr->rank < 0 || pr->rank >= pr->world)
+    return fail(CPA_ERR_SHAPE, "world %d / rank %d out of range (world <= %d)", pr->world, pr->rank, CPA_MAX_PEERS);
+  if (pr->epoch == 0) return fail(CPA_ERR_SHAPE, "epoch must be >= 1");
+  for (int w = 0; w < pr->world; ++w) {
+    if (!pr->peer_signal[w]) return fail(CPA_ERR_NULL, "peer_signal[%d] is NULL", w);
+    if (reinterpret_cast<uintptr_t>(pr->peer_signal[w]) & 3u) return fail(CPA_ERR_MISALIGNED, "peer_signal[%d]", w);
+  }
+  return CPA_OK;
+}
+
+int peer_barrier_impl(const cpa_peer_out* pr, cudaStream_t st) {
+  PeerSig sg;
+  for (int w = 0; w < kMaxOut; ++w) sg.pads[w] = w < pr->world ? pr->peer_signal[w] : nullptr;
+  sg.world = pr->world;
+  sg.rank = pr->rank;
+  sg.epoch = pr->epoch;
+  sg.status = pr->dev_status;
+  sg.timeout_ns = (unsigned long long)(pr->timeout_ms ? pr->timeout_ms : 10000u) * 1000000ull;
+  cudaError_t e = launch_peer_barrier(sg, st, &g_launches);
+  if (e != cudaSuccess) return cuda_fail(e, "peer_barrier");
+  return CPA_OK;
 }
 
 // NEXT-3 copy ablation: compact pool [B*Gn*nkvb pages] of K and of V + per-row page tables
@@ -368,30 +443,48 @@ int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chunk, cons
                    const cpa_kv_cache* cache, cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
                    void* stream) {
   g_launches = 0;
+  return chunk_step_impl(p, q, k_chunk, v_chunk, cache, tables, o, ws, ws_bytes, (cudaStream_t)stream, nullptr);
+}
+
+int cpa_chunk_step_peer(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                        const cpa_kv_cache* cache, cpa_tables* tables, const cpa_peer_out* peers, void* ws,
+                        size_t ws_bytes, void* stream) {
+  g_launches = 0;
   Geo g;
-  int s, sms;
-  long long ps, hs;
+  int s;
   if ((s = make_geo(p, &g)) != CPA_OK) return s;
-  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
-  if ((s = device_info(&sms)) != CPA_OK) return s;
-  if ((k_chunk == nullptr) != (v_chunk == nullptr)) return fail(CPA_ERR_NULL, "k_chunk/v_chunk: both or neither");
-  if (!q || !o) return fail(CPA_ERR_NULL, "q/o is NULL");
-  if (!tables) return fail(CPA_ERR_NULL, "tables is NULL");
-  int total = 0;
-  if (k_chunk) {
-    if (!aligned16(k_chunk) || !aligned16(v_chunk)) return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
-    cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, (cudaStream_t)stream, &g_launches);
-    if (e != cudaSuccess) return cuda_fail(e, "append");
+  if ((s = check_peers(peers)) != CPA_OK) return s;
+  if (!peers->peer_out) return fail(CPA_ERR_NULL, "peer_out is NULL");
+  const int W = peers->world;
+  const long long row = (long long)W * g.Hq * g.d;
+  OutSpec os;
+  os.n = W;
+  os.stride = peers->out_token_stride ? peers->out_token_stride : row;
+  if (os.stride < row || os.stride % 8) return fail(CPA_ERR_SHAPE, "out_token_stride must be >= W*Hq*d, multiple of 8");
+  os.bstride = (long long)g.C * os.stride;
+  const size_t esz = (p->flags & CPA_F_OUT_F32) ? 4 : 2;
+  for (int k = 0; k < W; ++k) {  // own buffer first, then the peers in rotated order (spreads NVLink load)
+    const int w = (peers->rank + k) % W;
+    if (!peers->peer_out[w]) return fail(CPA_ERR_NULL, "peer_out[%d] is NULL", w);
+    if (!aligned16(peers->peer_out[w])) return fail(CPA_ERR_MISALIGNED, "peer_out[%d] not 16B aligned", w);
+    os.outs[k] = reinterpret_cast<uint8_t*>(peers->peer_out[w]) + (size_t)peers->rank * g.Hq * g.d * esz;
   }
-  total += g_launches;
-  g_launches = 0;
-  if ((s = build_tables_impl(p, g, q, cache, ps, hs, tables, ws, ws_bytes, (cudaStream_t)stream, sms)) != CPA_OK)
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = chunk_step_impl(p, q, k_chunk, v_chunk, cache, tables, nullptr, ws, ws_bytes, st, &os)) != CPA_OK)
     return s;
-  total += g_launches;
+  const int n = g_launches;
   g_launches = 0;
-  if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream)) != CPA_OK) return s;
-  g_launches += total;
+  if ((s = peer_barrier_impl(peers, st)) != CPA_OK) return s;
+  g_launches += n;
   return CPA_OK;
+}
+
+int cpa_peer_barrier(const cpa_peer_out* peers, void* stream) {
+  g_launches = 0;
+  int s, sms;
+  if ((s = check_peers(peers)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  return peer_barrier_impl(peers, (cudaStream_t)stream);
 }
 
 size_t cpa_copy_workspace_bytes(const cpa_params* p) {

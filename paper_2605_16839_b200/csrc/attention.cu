@@ -21,6 +21,7 @@
 // domain with lazy O rescaling (only when the running max grows by > 8, so P <= 256).
 #include "common.cuh"
 #include "geo.cuh"
+#include "out_store.cuh"
 
 namespace cpa {
 
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
       mbar_wait(o_full, 0);
       tc_fence_after();
     }
-    const long long obase = (long long)b * g.b_stride + (long long)p * g.q_stride + (long long)h * D;
+    const long long obase = (long long)b * args.o_bstride + (long long)p * args.o_stride + (long long)h * D;
 #pragma unroll
     for (int c0 = 0; c0 < D; c0 += 32) {
       uint32_t o[32];
@@ -449,23 +450,10 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
 #pragma unroll
         for (int c = 0; c < 32; ++c) o[c] = 0u;
       }
-      if (store) {
-        if (args.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + obase + c0);
+      float v[32];
 #pragma unroll
-          for (int c = 0; c < 32; c += 4)
-            dst[c / 4] = make_float4(__uint_as_float(o[c]) * inv_l, __uint_as_float(o[c + 1]) * inv_l,
-                                     __uint_as_float(o[c + 2]) * inv_l, __uint_as_float(o[c + 3]) * inv_l);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + obase + c0);
-#pragma unroll
-          for (int c = 0; c < 32; c += 8)
-            dst[c / 8] = make_uint4(pack_bf16x2(__uint_as_float(o[c]) * inv_l, __uint_as_float(o[c + 1]) * inv_l),
-                                    pack_bf16x2(__uint_as_float(o[c + 2]) * inv_l, __uint_as_float(o[c + 3]) * inv_l),
-                                    pack_bf16x2(__uint_as_float(o[c + 4]) * inv_l, __uint_as_float(o[c + 5]) * inv_l),
-                                    pack_bf16x2(__uint_as_float(o[c + 6]) * inv_l, __uint_as_float(o[c + 7]) * inv_l));
-        }
-      }
+      for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(o[c]) * inv_l;
+      if (store) store_o_row32(args, obase + c0, v);
     }
   }
   tc_fence_before();

@@ -18,6 +18,7 @@
 // 10 TMA producer, 11 TMEM alloc + MMA issuer.
 #include "common.cuh"
 #include "geo.cuh"
+#include "out_store.cuh"
 
 namespace cpa {
 
@@ -386,7 +387,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       tc_fence_after();
     }
     const uint32_t ob0 = tmem + lane_off + 256 + wg * (D / 2), ob1 = ob0 + 128;
-    const long long obase = (long long)b * g.b_stride + (long long)p * g.q_stride + (long long)h * D + wg * (D / 2);
+    const long long obase =
+        (long long)b * args.o_bstride + (long long)p * args.o_stride + (long long)h * D + wg * (D / 2);
 #pragma unroll
     for (int cc = 0; cc < D / 2; cc += 32) {
       uint32_t o0[32], o1[32];
@@ -397,19 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
       for (int c = 0; c < 32; ++c)
         v[c] = (has0 ? __uint_as_float(o0[c]) * c0f : 0.f) + (has1 ? __uint_as_float(o1[c]) * c1f : 0.f);
-      if (store) {
-        if (args.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(args.out) + obase + cc);
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) dst[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.out) + obase + cc);
-#pragma unroll
-          for (int c = 0; c < 32; c += 8)
-            dst[c / 8] = make_uint4(pack_bf16x2(v[c], v[c + 1]), pack_bf16x2(v[c + 2], v[c + 3]),
-                                    pack_bf16x2(v[c + 4], v[c + 5]), pack_bf16x2(v[c + 6], v[c + 7]));
-        }
-      }
+      if (store) store_o_row32(args, obase + cc, v);
     }
   }
   tc_fence_before();

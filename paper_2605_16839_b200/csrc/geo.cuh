@@ -27,13 +27,30 @@ __host__ __device__ inline int group_kv_head(const Geo& g, int grp) {
 //                       1-CTA kernel only; mask layout [B, Hq, nqb, nwords] u32, LSB-first);
 //   indptr  != nullptr: its CSR table row b*Gn + g (zero-copy paged execution);
 //   else               every block (dense baseline).
+// Output: the normalised O tile of every CTA is stored to each of outs[0 .. n_out): outs[0] is the
+// call's own output; with a peer exchange (cpa_chunk_step_peer) outs[k] is rank (rank+k) % W's
+// gathered buffer, already offset to this rank's head slice and mapped into this process (P2P over
+// NVLink), so the all-gather of the head outputs happens in the epilogue, tile by tile.
+constexpr int kMaxOut = 8;
 struct AttnArgs {
   const int32_t* page_table;
   const int32_t* indptr;
   const int32_t* indices;
   const uint32_t* mask;
-  void* out;
   int out_f32;
+  int n_out;             // >= 1
+  long long o_stride;    // elements between tokens of every output
+  long long o_bstride;   // elements between batch entries of every output
+  void* outs[kMaxOut];
+};
+
+// Arguments of the peer completion barrier (peer.cu).
+struct PeerSig {
+  uint32_t* pads[kMaxOut];  // pads[w]: rank w's signal pad u32[W], mapped into this process
+  int world, rank;
+  uint32_t epoch;
+  int* status;              // optional: 1 + the peer that did not arrive within the timeout
+  unsigned long long timeout_ns;
 };
 
 }  // namespace cpa

@@ -74,3 +74,26 @@ def test_capacity_and_geometry(L):
     p = _p()
     nqb, nkvb, pb, Gn, nwords, Rpad = cpa.geometry(p)
     assert (nqb, nkvb, pb, Gn, nwords, Rpad) == (32, 1024, 992, 8, 32, 128)
+
+
+def _peer(world, rank, outs=16, sigs=16, epoch=1, stride=0):
+    o = (ctypes.c_void_p * max(world, 1))(*([outs] * max(world, 1)))
+    s = (ctypes.c_void_p * max(world, 1))(*([sigs] * max(world, 1)))
+    return cpa._PeerOut(world, rank, o if outs is not None else None, stride, s if sigs is not None else None,
+                        epoch, 0, None), (o, s)
+
+
+@pytest.mark.parametrize("world,rank,kw,status", [
+    (0, 0, {}, 2), (9, 0, {}, 2), (2, 2, {}, 2), (2, -1, {}, 2), (2, 0, dict(epoch=0), 2),
+    (2, 0, dict(sigs=None), 1), (2, 0, dict(outs=None), 1), (2, 0, dict(sigs=0), 1), (2, 0, dict(sigs=18), 4),
+    (2, 0, dict(outs=24), 4), (2, 0, dict(stride=100), 2),
+])
+def test_peer_validation(L, world, rank, kw, status):
+    """cpa_chunk_step_peer validates the peer description before touching the device (cpa.h)."""
+    p = _p(num_q_heads=16, num_kv_heads=4)  # one rank's shard of the LLaMA shape at W=2
+    pr, keep = _peer(world, rank, **kw)
+    c = cpa._Cache(16, 16, 0, 0, 16, 2048, 10)
+    t = cpa._Tables(16, 16, 1 << 20, None, None, None, None)
+    r = L.cpa_chunk_step_peer(ctypes.byref(p), 16, None, None, ctypes.byref(c), ctypes.byref(t), ctypes.byref(pr),
+                              16, 1 << 30, None)
+    assert r == status, L.cpa_last_error()

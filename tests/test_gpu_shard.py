@@ -55,3 +55,58 @@ def test_sharded_equals_unsharded(cfg_name, world):
                 rl = b * per + gl
                 assert np.array_equal(ix[ip[rl]:ip[rl + 1]], ix_ref[ip_ref[G]:ip_ref[G + 1]])
     assert torch.equal(o_sh, o_ref)
+
+
+@pytest.mark.parametrize("cfg_name,world,f32", [("tiny", 2, True), ("llama8b_32k", 2, False),
+                                                ("llama8b_32k", 4, False), ("llama8b_32k", 8, False)])
+def test_fused_peer_allgather(cfg_name, world, f32):
+    """cpa_chunk_step_peer on W simulated ranks of one GPU (each rank on its own stream, its peers'
+    gathered buffers and signal pads plain device tensors, so the P2P stores are local stores): every
+    rank's gathered buffer [B, C, Hq, d] must equal the unsharded chunk step bit for bit, and the
+    barrier must complete (dev_status 0) for several consecutive epochs."""
+    cfg = CONFIGS[cfg_name]
+    seed = 16839
+    k, v = make_kv(cfg, seed)
+    q = to_dev_bf16(make_q(cfg, seed))
+    P, C, L = cfg.chunk_geometry()
+    bs, d, Hq = cfg.block_size, cfg.head_dim, cfg.num_q_heads
+    dt = torch.float32 if f32 else torch.bfloat16
+    shape = (cfg.batch, C, Hq, d)
+    nkvb = -(-L // bs)
+    # unsharded reference
+    pt, npages = page_layout(cfg.batch, nkvb, seed)
+    cache = cpa.PagedKVCache(to_dev_bf16(to_pool(k, pt, npages, bs)), to_dev_bf16(to_pool(v, pt, npages, bs)),
+                             torch.from_numpy(pt).cuda())
+    pf = cpa.make_params(cfg.batch, Hq, cfg.num_kv_heads, d, bs, C, P, alpha=0.06,
+                         flags=cpa.F_OUT_F32 if f32 else 0)
+    o_ref = torch.empty(shape, dtype=dt, device="cuda")
+    cpa.chunk_step(pf, q, cache, cpa.alloc_tables(pf), o_ref)
+    torch.cuda.synchronize()
+    # W ranks: own shard of the pool, own q slice (contiguous copy, as a rank would hold it)
+    outs = [torch.full(shape, float("nan"), dtype=dt, device="cuda") for _ in range(world)]
+    pads = [torch.zeros(world, dtype=torch.int32, device="cuda") for _ in range(world)]
+    status = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(world)]
+    ranks = []
+    for r in range(world):
+        kvh, qh = head_shard(Hq, cfg.num_kv_heads, world, r)
+        ptr, npr = page_layout(cfg.batch, nkvb, seed + 7 * r)
+        kk, vv = k[:, kvh.start:kvh.stop], v[:, kvh.start:kvh.stop]
+        c = cpa.PagedKVCache(to_dev_bf16(to_pool(kk, ptr, npr, bs)), to_dev_bf16(to_pool(vv, ptr, npr, bs)),
+                             torch.from_numpy(ptr).cuda())
+        p = cpa.make_params(cfg.batch, len(qh), len(kvh), d, bs, C, P, alpha=0.06,
+                            flags=cpa.F_OUT_F32 if f32 else 0)
+        peers = cpa.PeerOut(world, r, [o.data_ptr() for o in outs], [x.data_ptr() for x in pads],
+                            timeout_ms=5000, dev_status=status[r])
+        ranks.append((p, q[:, :, qh.start:qh.stop].contiguous(), c, cpa.alloc_tables(p), peers,
+                      torch.cuda.Stream(), torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")))
+    for epoch in range(3):
+        for o in outs:
+            o.fill_(float("nan"))
+        torch.cuda.synchronize()
+        for p, qr, c, t, peers, st, ws in ranks:  # each rank owns its workspace, like a real rank
+            cpa.chunk_step_peer(p, qr, c, t, peers, workspace=ws, stream=st)
+        torch.cuda.synchronize()
+        assert [int(s.item()) for s in status] == [0] * world
+        assert all(int(x) == epoch + 1 for pad in pads for x in pad.cpu())
+        for w in range(world):
+            assert torch.equal(outs[w], o_ref), (epoch, w)
