@@ -36,7 +36,13 @@ struct Attn2Cfg {
   static constexpr int kQBytes = 128 * D * 2;           // this CTA's Q tile
   static constexpr int kKHalf = (BS / 2) * D * 2;       // half of a K page (keys)
   static constexpr int kVHalf = BS * 64 * 2;            // half of a V page (head-dim columns)
-  static constexpr int kKStages = 4, kVStages = 4;
+#ifndef CPA_KSTAGES
+#define CPA_KSTAGES 4
+#endif
+#ifndef CPA_VSTAGES
+#define CPA_VSTAGES 4
+#endif
+  static constexpr int kKStages = CPA_KSTAGES, kVStages = CPA_VSTAGES;
   static constexpr int kConvWarps = 2;
   static constexpr int kThreads = 12 * 32;       // 8 softmax + 2 converter + TMA + MMA warps
   static constexpr int kSmem = kQBytes + kKStages * kKHalf + kVStages * kVHalf + 1024 + 512;
@@ -294,6 +300,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_wait(s_full + (n & 1), (n >> 1) & 1);
       if (row == 0) TRACE2(5 + 16 * wg, n);
       tc_fence_after();
+#ifdef CPA_EXP_NO_SOFTMAX  // A/B only: MMA / TMA / converter pipeline alone (wrong results)
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
+      continue;
+#endif
       uint32_t sv[HC / 32][32];
 #pragma unroll
       for (int k = 0; k < HC / 32; ++k) tmem_ld32(s_tm + k * 32, sv[k]);

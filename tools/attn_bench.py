@@ -25,8 +25,12 @@ import ctypes
 tabs = None
 times = {(v_, n_): [] for v_ in variants for n_ in ("sparse", "dense")}
 ref = None
+import random
+rng = random.Random(0)
 for r in range(rounds):
-    for (path, fl) in variants:
+    order = list(variants)
+    rng.shuffle(order)  # no variant always follows the same one (power / clock carry-over)
+    for (path, fl) in order:
         cpa._lib = libs.get(path); cpa.LIB_PATH = path
         cpa.lib(); libs[path] = cpa._lib
         p.flags = (p.flags & 1) | fl
@@ -45,4 +49,5 @@ for r in range(rounds):
 for (path, fl) in variants:
     print(json.dumps({"lib": os.path.basename(path), "flags": fl,
                       "sparse_ms": round(float(np.median(times[((path, fl), "sparse")])), 4),
+                      "sparse_min_ms": round(float(np.min(times[((path, fl), "sparse")])), 4),
                       "dense_ms": round(float(np.median(times[((path, fl), "dense")])), 4)}), flush=True)

@@ -26,17 +26,20 @@ d = lambda a, b: int(a - b)
 per = [d(tr[2, n + 1], tr[2, n]) for n in range(2, N - 2)]
 print("blocks", N, "median period per 128-key page (cycles)", int(np.median(per)))
 for n in list(range(0, 4)) + list(range(N // 2, N // 2 + 4)):
-    print(json.dumps({"n": n, "period": d(tr[2, n + 1], tr[2, n]) if n + 1 < N else 0,
-        "mma_vready_wait": d(tr[1, n], tr[3, n - 1]) if n > 0 else 0, "mma_p_wait": d(tr[2, n], tr[1, n]),
-        "mma_pv_issue": d(tr[9, n], tr[2, n]), "mma_k_wait": d(tr[10, n], tr[9, n]), "mma_s_issue": d(tr[3, n], tr[10, n]),
-        "wg": n % 2, "sm_wait": d(tr[5 + 16*(n%2), n], tr[4 + 16*(n%2), n]),
-        "sm_ld_max": d(tr[11 + 16*(n%2), n], tr[5 + 16*(n%2), n]), "sm_exp": d(tr[12 + 16*(n%2), n], tr[11 + 16*(n%2), n]),
-        "sm_tail": d(tr[6 + 16*(n%2), n], tr[12 + 16*(n%2), n]), "conv": d(tr[8, n], tr[7, n])}))
+    rec = {"n": n, "period": d(tr[2, n + 1], tr[2, n]) if n + 1 < N else 0,
+           "mma_vready_wait": d(tr[1, n], tr[3, n - 1]) if n > 0 else 0, "mma_p_wait": d(tr[2, n], tr[1, n]),
+           "mma_pv_issue": d(tr[9, n], tr[2, n]), "mma_k_wait": d(tr[10, n], tr[9, n]),
+           "mma_s_issue": d(tr[3, n], tr[10, n]), "conv": d(tr[8, n], tr[7, n])}
+    for w in (0, 1):  # both softmax WGs work on every page (key-column halves)
+        o_ = 16 * w
+        rec[f"wg{w}"] = {"wait": d(tr[5 + o_, n], tr[4 + o_, n]), "ld_max": d(tr[11 + o_, n], tr[5 + o_, n]),
+                         "exp": d(tr[12 + o_, n], tr[11 + o_, n]), "tail": d(tr[6 + o_, n], tr[12 + o_, n])}
+    print(json.dumps(rec))
 # absolute timeline (cycles from the first listed event) of a few mid-kernel pages
 b0 = N // 2
-t0 = int(tr[5 + 16 * (b0 % 2), b0])
+t0 = int(tr[5, b0])
 for n in range(b0, b0 + 6):
-    w = n % 2
     r = lambda e: int(tr[e, n]) - t0
-    print(f"page {n} wg{w}: s_ready {r(5 + 16*w):6d}  max_done {r(11 + 16*w):6d}  exp_done {r(12 + 16*w):6d}  "
-          f"p_arrive {r(6 + 16*w):6d} | mma: p_seen {r(2):6d} pv_issued {r(9):6d} s(n+2)_issued {r(3):6d}")
+    print(f"page {n}: " + " | ".join(
+        f"wg{w} s_ready {r(5 + 16*w):6d} max {r(11 + 16*w):6d} exp {r(12 + 16*w):6d} arrive {r(6 + 16*w):6d}"
+        for w in (0, 1)) + f" || mma: p_seen {r(2):6d} pv_issued {r(9):6d} s(n+2)_issued {r(3):6d}")
