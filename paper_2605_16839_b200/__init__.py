@@ -18,7 +18,7 @@ __all__ = [
     "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
     "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
     "paged_attention_copy", "block_sparse_attention", "expand_tables", "PeerOut", "chunk_step_peer",
-    "peer_barrier",
+    "peer_barrier", "HostChunkStream",
     "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "EXPORTED_SYMBOLS",
 ]
 
@@ -301,6 +301,56 @@ def expand_tables(p: Params, tables: BlockTables, mask_bits: torch.Tensor, strea
     t = tables._c()
     _check(lib().cpa_expand_tables(ctypes.byref(p), ctypes.byref(t), _ptr(mask_bits), _stream(stream)))
     return mask_bits
+
+
+class HostChunkStream:
+    """Chunk steps fed from pinned HOST buffers, pipelined over three streams: the H2D copy of step
+    i+1's inputs and the D2H copy of step i-1's output overlap step i's kernels (device staging is
+    double-buffered; the cache, tables and workspace are used in stream order on the compute stream).
+    Plumbing only -- every step runs cpa_chunk_step. Read a host output only after synchronize()."""
+
+    def __init__(self, p: Params, cache: PagedKVCache, tables: BlockTables, q_shape, kv_shape,
+                 workspace: Optional[torch.Tensor] = None, device="cuda"):
+        self.p, self.cache, self.tables = p, cache, tables
+        self.ws = workspace if workspace is not None else _ws(p, None, device)
+        bf = torch.bfloat16
+        o_dtype = torch.float32 if p.flags & F_OUT_F32 else bf
+        self.q = [torch.empty(q_shape, dtype=bf, device=device) for _ in range(2)]
+        self.k = [torch.empty(kv_shape, dtype=bf, device=device) for _ in range(2)]
+        self.v = [torch.empty(kv_shape, dtype=bf, device=device) for _ in range(2)]
+        self.o = [torch.empty(q_shape, dtype=o_dtype, device=device) for _ in range(2)]
+        self.s_in, self.s_comp, self.s_out = (torch.cuda.Stream(device) for _ in range(3))
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+
+    def submit(self, hq: torch.Tensor, ho: torch.Tensor, hk: Optional[torch.Tensor] = None,
+               hv: Optional[torch.Tensor] = None) -> None:
+        """Enqueue one chunk step: hq [B,C,Hq,d] (+ hk/hv [B,C,Hkv,d] to append) -> ho [B,C,Hq,d]."""
+        s = self.i & 1
+        self.s_in.wait_event(self.ev_comp[s])        # step i-2 has finished reading this slot
+        with torch.cuda.stream(self.s_in):
+            self.q[s].copy_(hq, non_blocking=True)
+            if hk is not None:
+                self.k[s].copy_(hk, non_blocking=True)
+                self.v[s].copy_(hv, non_blocking=True)
+            self.ev_in[s].record(self.s_in)
+        self.s_comp.wait_event(self.ev_in[s])
+        self.s_comp.wait_event(self.ev_out[s])       # D2H of step i-2 has finished reading o[s]
+        chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s],
+                   self.k[s] if hk is not None else None, self.v[s] if hk is not None else None,
+                   workspace=self.ws, stream=self.s_comp)
+        self.ev_comp[s].record(self.s_comp)
+        self.s_out.wait_event(self.ev_comp[s])
+        with torch.cuda.stream(self.s_out):
+            ho.copy_(self.o[s], non_blocking=True)
+            self.ev_out[s].record(self.s_out)
+        self.i += 1
+
+    def synchronize(self) -> None:
+        for st in (self.s_in, self.s_comp, self.s_out):
+            st.synchronize()
 
 
 def last_launch_count() -> int:
