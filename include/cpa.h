@@ -77,7 +77,9 @@ enum {
   CPA_F_EXACT_SCORES = 32u, /* SPEC.md:223 exact tile-max scorer (full QK^T, max over every causal
                                (p, t) pair of the tile) instead of the pooled-query estimator */
   CPA_F_P_BF16 = 256u,    /* ablation: round softmax P to bf16 instead of fp16 before P.V (K3) */
-  CPA_F_NO_2CTA = 512u    /* ablation: single-CTA attention kernel instead of the cta_group::2 pair */
+  CPA_F_NO_2CTA = 512u,   /* ablation: single-CTA attention kernel instead of the cta_group::2 pair */
+  CPA_F_NO_PERSIST = 1024u, /* ablation: one cluster per work unit instead of the persistent stream-K grid */
+  CPA_F_PERSIST = 2048u   /* ablation / tests: persistent stream-K grid whenever B*Gn <= 4 */
 };
 
 typedef struct {
@@ -132,7 +134,8 @@ typedef struct {
                             mask lacks a chunk block (open-chunk violation); 0 otherwise */
 } cpa_tables;
 
-/* Device workspace needed by cpa_build_tables / cpa_paged_attention / cpa_chunk_step. */
+/* Device workspace needed by cpa_build_tables / cpa_paged_attention / cpa_chunk_step (the estimator
+ * scratch and the attention's stream-K schedule + partial-output slots share one buffer). */
 CPA_API size_t cpa_workspace_bytes(const cpa_params* p);
 
 /* Stages (1)+(2): estimator -> M -> Q-block union -> intra-group union -> CSR tables.
@@ -149,7 +152,15 @@ CPA_API int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_ca
 /* Stage (3): O[b,p,h] = sum_{t in A(p)} softmax_t(sm_scale q_p . k_t) v_t with
  *   A(p) = { t : floor(t/bs) in T[b, h/E], t <= P + p }  (absolute coordinates).
  *   tables == NULL => dense causal chunk attention over every block [0, nkvb) (the baseline).
- *   o: bf16 (or fp32 with CPA_F_OUT_F32) [B, C, Hq, d], token stride p->q_token_stride. */
+ *   o: bf16 (or fp32 with CPA_F_OUT_F32) [B, C, Hq, d], token stride p->q_token_stride.
+ *   ws: >= cpa_workspace_bytes(p) (CPA_ERR_WORKSPACE otherwise). When the work units (b, group,
+ *   128-token q-tile, head pair) do not fill whole waves of SM pairs and there are at most 4
+ *   (b, group) rows (e.g. one rank's KV-group shard), the cta_group::2 path runs a persistent grid of
+ *   one cluster per co-resident SM pair, each taking an equal contiguous share of every row's
+ *   (unit, page) work, and merges units cut by a share boundary in a fixup kernel; otherwise one
+ *   cluster per unit (the persistent grid is also skipped for KV shorter than 512 blocks, where the
+ *   shares are too short to amortise the per-item epilogue). CPA_F_NO_PERSIST / CPA_F_PERSIST force
+ *   either grid. */
 CPA_API int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
                         const cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
                         void* stream);

@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/cpa.h"
@@ -27,8 +28,10 @@ cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& 
 cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 bool attn_2cta_supported(const Geo& g);
+int attn_2cta_max_clusters(const Geo& g);
 cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
-                                        const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
+                                        const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st,
+                                        int* launches);
 cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g,
                           long long page_stride, long long head_stride, cudaStream_t st, int* launches);
 cudaError_t launch_gather_pages(const cpa_kv_cache& c, const int32_t* indptr, const int32_t* indices, const Geo& g,
@@ -203,6 +206,57 @@ WS carve(const Geo& g, void* base) {
   return w;
 }
 
+// Persistent stream-K attention (attention_2cta.cu). Its workspace (schedule + partial slots) is
+// carved from the start of ws: the chunk step runs the estimator first, so both stages share one
+// buffer. kSkMaxClusters bounds the persistent grid (B200: 74 co-resident SM pairs).
+// Policy: the per-unit grid already keeps every SM pair busy when the unit count fills whole waves
+// (128K, one GPU: 512 units = 6.92 waves of 74, 98.8%); stream-K pays off when it does not (one KV
+// group per GPU: 64 units on 74 pairs, 86%) and the (b, group) segments are few (every segment
+// boundary costs partial outputs: 2 per cluster per segment).
+constexpr int kSkMaxClusters = 80;
+static_assert(kSkFixStride - 2 >= kSkMaxClusters, "fixup part list holds one part per cluster");
+constexpr int kSkMaxSegments = 4;
+int sk_units(const Geo& g) { return (g.C + 127) / 128 * g.B * g.Gn * (g.E / 2); }
+int sk_segments(const Geo& g) { return g.B * g.Gn; }
+bool sk_wanted(const Geo& g, int clusters) {
+  if (g.flags & CPA_F_PERSIST) return sk_segments(g) <= kSkMaxSegments;
+  // short KV (< 64K tokens): shares are too short to amortise the per-item epilogue (measured:
+  // 32K, 2 KV groups, 8% slower than the per-unit grid; 128K, 1 KV group, 10% faster)
+  if (sk_segments(g) > kSkMaxSegments || g.nkvb < 512) return false;
+  const double waves = (double)sk_units(g) / clusters;
+  return waves / ceil(waves) < 0.9;
+}
+size_t attn_ws_bytes(const Geo& g) {
+  if (sk_segments(g) > kSkMaxSegments) return 0;
+  const size_t U = (size_t)sk_units(g), slots = (size_t)kSkMaxClusters * sk_segments(g) * 2;
+  return 4 * up256((U + 1) * 4) + up256(slots * 256 * g.d * 4) + up256(slots * 256 * 2 * 4) +
+         up256((size_t)kSkMaxClusters * sk_segments(g) * kSkFixStride * 4);
+}
+SkSched carve_sk(const Geo& g, void* base, int clusters) {
+  SkSched s;
+  const size_t U = (size_t)sk_units(g);
+  uint8_t* p = reinterpret_cast<uint8_t*>(base);
+  s.pre = reinterpret_cast<int*>(p);
+  p += up256((U + 1) * 4);
+  s.len = reinterpret_cast<int*>(p);
+  p += up256((U + 1) * 4);
+  s.start = reinterpret_cast<int*>(p);
+  p += up256((U + 1) * 4);
+  s.nd = reinterpret_cast<int*>(p);
+  p += up256((U + 1) * 4);
+  const size_t slots = (size_t)kSkMaxClusters * sk_segments(g) * 2;
+  s.part_o = reinterpret_cast<float*>(p);
+  p += up256(slots * 256 * g.d * 4);
+  s.part_ml = reinterpret_cast<float*>(p);
+  p += up256(slots * 256 * 2 * 4);
+  s.fix = reinterpret_cast<int*>(p);
+  s.units = (int)U;
+  s.clusters = clusters;
+  s.segments = sk_segments(g);
+  s.seg_units = (int)U / s.segments;
+  return s;
+}
+
 int q_map(CUtensorMap* m, const void* q, const Geo& g) {
   cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.Hq, (cuuint64_t)g.C, (cuuint64_t)g.B};
   cuuint64_t str[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.q_stride * 2, (cuuint64_t)g.b_stride * 2};
@@ -282,7 +336,7 @@ struct OutSpec {
 int attention_launch(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
                      int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
                      const int32_t* indices, void* o, cudaStream_t st, const uint32_t* mask = nullptr,
-                     const OutSpec* os = nullptr) {
+                     const OutSpec* os = nullptr, void* ws = nullptr, size_t ws_bytes = 0) {
   CUtensorMap tq, tk, tv;
   int s;
   if ((s = q_map(&tq, q, g)) != CPA_OK) return s;
@@ -310,7 +364,14 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
   if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA) && mask == nullptr) {
     CUtensorMap tkh;  // half a page of keys per CTA of the pair
     if ((s = kv_map(&tkh, k_pages, g, num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
-    e = launch_paged_attention_2cta(tq, tkh, tv, g, a, st, &g_launches);
+    const int clusters = std::min(attn_2cta_max_clusters(g), kSkMaxClusters);
+    if (ws != nullptr && !(p->flags & CPA_F_NO_PERSIST) && sk_wanted(g, clusters)) {  // persistent stream-K
+      if (ws_bytes < attn_ws_bytes(g)) return fail(CPA_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, attn_ws_bytes(g));
+      SkSched sk = carve_sk(g, ws, clusters);
+      e = launch_paged_attention_2cta(tq, tkh, tv, g, a, &sk, st, &g_launches);
+    } else {
+      e = launch_paged_attention_2cta(tq, tkh, tv, g, a, nullptr, st, &g_launches);
+    }
   } else {
     e = launch_paged_attention(tq, tk, tv, g, a, st, &g_launches);
   }
@@ -319,12 +380,16 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
 }
 
 int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
-                   long long hs, const cpa_tables* t, void* o, cudaStream_t st, const OutSpec* os = nullptr) {
+                   long long hs, const cpa_tables* t, void* o, cudaStream_t st, const OutSpec* os, void* ws,
+                   size_t ws_bytes) {
   if (!q || (!o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
   if (!aligned16(q) || (!os && !aligned16(o))) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
   if (t && (!t->kv_indptr || !t->kv_indices)) return fail(CPA_ERR_NULL, "tables pointers");
+  if (attn_2cta_supported(g) && !(p->flags & (CPA_F_NO_2CTA | CPA_F_NO_PERSIST)) && attn_ws_bytes(g) > 0 &&
+      ws_bytes < attn_ws_bytes(g))
+    return fail(CPA_ERR_WORKSPACE, "paged attention needs cpa_workspace_bytes() of workspace");
   return attention_launch(p, g, q, c->k_pages, c->v_pages, c->num_pages, ps, hs, c->page_table,
-                          t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, st, nullptr, os);
+                          t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, st, nullptr, os, ws, ws_bytes);
 }
 
 // append (optional) -> estimator + tables -> attention, the body of cpa_chunk_step(_peer)
@@ -351,7 +416,7 @@ int chunk_step_impl(const cpa_params* p, const void* q, const void* k_chunk, con
   if ((s = build_tables_impl(p, g, q, cache, ps, hs, tables, ws, ws_bytes, st, sms)) != CPA_OK) return s;
   total += g_launches;
   g_launches = 0;
-  if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, st, os)) != CPA_OK) return s;
+  if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, st, os, ws, ws_bytes)) != CPA_OK) return s;
   g_launches += total;
   return CPA_OK;
 }
@@ -394,7 +459,7 @@ extern "C" {
 size_t cpa_workspace_bytes(const cpa_params* p) {
   Geo g;
   if (make_geo(p, &g) != CPA_OK) return 0;
-  return carve(g, nullptr).total;
+  return std::max(carve(g, nullptr).total, attn_ws_bytes(g));
 }
 
 int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_cache* cache, cpa_tables* out,
@@ -411,8 +476,6 @@ int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_cache* cac
 
 int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache, const cpa_tables* tables,
                         void* o, void* ws, size_t ws_bytes, void* stream) {
-  (void)ws;
-  (void)ws_bytes;
   g_launches = 0;
   Geo g;
   int s, sms;
@@ -420,7 +483,7 @@ int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* 
   if ((s = make_geo(p, &g)) != CPA_OK) return s;
   if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
   if ((s = device_info(&sms)) != CPA_OK) return s;
-  return attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream);
+  return attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream, nullptr, ws, ws_bytes);
 }
 
 int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk, const cpa_kv_cache* cache,

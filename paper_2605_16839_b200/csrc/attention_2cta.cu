@@ -4,15 +4,24 @@
 //   O[b,p,h] = sum_{t in A(p)} softmax_t(scale q_p.k_t) v_t,  A(p) = {t : t/bs in T[b,h/E], t <= P+p}
 // with causal masking in absolute positions.
 //
-// Cluster of 2 CTAs = (b, group g, 128-token q-tile, head pair {h0, h0+1} of g). CTA r holds the
-// 128 query rows of head h0+r; every tcgen05.mma is M=256 (both CTAs' rows) and issued by CTA 0.
-// Each page is split across the pair: CTA r loads keys [r*bs/2, (r+1)*bs/2) of K and head-dim
-// columns [64r, 64r+64) of V, so per SM the tensor core reads 6 KB of shared memory per 64-cycle
-// S MMA (96 B/clk, under the 128 B/clk limit that caps a 1-CTA 128x128 SS MMA) and the TMA / L2
-// traffic per FLOP halves. P (fp16) aliases S^b; the MMA computes S(n+1) while the softmax of S(n)
-// runs. Both softmax warpgroups work on every page: WG w owns key columns [w BS/2, (w+1) BS/2) of
-// each S^b and keeps its own running max / sum and accumulator O_w (P.V of its half of the keys),
-// so the two WGs never exchange anything per page; the epilogue merges (m_w, l_w, O_w).
+// Work unit u = (b, group g, 128-token q-tile, head pair {h0, h0+1} of g) over the unit's visible
+// table prefix (N_u pages). CTA r of the pair holds the 128 query rows of head h0+r; every
+// tcgen05.mma is M=256 (both CTAs' rows) and issued by CTA 0. Each page is split across the pair:
+// CTA r loads keys [r*bs/2, (r+1)*bs/2) of K and head-dim columns [64r, 64r+64) of V, so per SM the
+// tensor core reads 6 KB of shared memory per 64-cycle S MMA (96 B/clk, under the 128 B/clk limit
+// that caps a 1-CTA 128x128 SS MMA) and the TMA / L2 traffic per FLOP halves. P (fp16) aliases S^b;
+// the MMA computes S(n+1) while the softmax of S(n) runs. Both softmax warpgroups work on every page:
+// WG w owns key columns [w BS/2, (w+1) BS/2) of each S^b and keeps its own running max / sum and
+// accumulator O_w (P.V of its half of the keys); the epilogue merges (m_w, l_w, O_w).
+//
+// Scheduling. Non-persistent (sched == nullptr): one cluster per unit, heaviest q-tile first within
+// an execution group (group-major, so the clusters in flight share few groups' KV pages in L2).
+// Persistent stream-K (sched != nullptr, see k_sk_schedule): one cluster per co-resident SM pair;
+// the concatenated page lists of all units (same order) are cut into equal contiguous ranges, so
+// every cluster gets the same number of pages whatever the unit count (no wave quantisation: e.g.
+// 64 units on 74 SM pairs at one KV group per GPU). A cluster walks its items (unit, page range);
+// the K/V / S / P pipelines run continuously across items, Q is double-buffered; a unit cut by a
+// range boundary is written as unnormalised partials (O, m, l) and merged by k_sk_fixup.
 // TMEM per CTA: S^0 [0,128) S^1 [128,256) O_0 [256,384) O_1 [384,512).
 // Warps: 0-7 softmax (WG = warp/4, lane quarter = warp%4), 8-9 V bf16->fp16 converters,
 // 10 TMA producer, 11 TMEM alloc + MMA issuer.
@@ -45,24 +54,209 @@ struct Attn2Cfg {
   static constexpr int kKStages = CPA_KSTAGES, kVStages = CPA_VSTAGES;
   static constexpr int kConvWarps = 2;
   static constexpr int kThreads = 12 * 32;       // 8 softmax + 2 converter + TMA + MMA warps
-  static constexpr int kSmem = kQBytes + kKStages * kKHalf + kVStages * kVHalf + 1024 + 512;
-  static_assert(kSmem <= 232448, "shared memory budget");
+  static constexpr int kSmem = 2 * kQBytes + kKStages * kKHalf + kVStages * kVHalf + 1024 + 512;
+  static_assert(kSmem + 2048 <= 232448, "shared memory budget");
+};
+
+// Coordinates of work unit u (cluster order of the non-persistent grid).
+struct Unit {
+  int b, grp, qt, hp;
+};
+__device__ __forceinline__ Unit unit_coords(const Geo& g, int u) {
+  const int HP = g.E / 2, nqt = (g.C + 127) / 128;
+  Unit r;
+  r.hp = u % HP;
+  r.qt = nqt - 1 - (u / HP) % nqt;
+  const int bg = u / (HP * nqt);
+  r.grp = bg % g.Gn;
+  r.b = bg / g.Gn;
+  return r;
+}
+
+// Visible table prefix of unit u: first entry `start`, `n` entries with block <= the tile's last
+// query position, of which the first `nd` are fully visible to every row (no causal mask).
+__device__ __forceinline__ void unit_table(const Geo& g, const AttnArgs& args, int u, int* start, int* n, int* nd) {
+  const Unit c = unit_coords(g, u);
+  const int p0 = c.qt * 128;
+  const int jmax = (g.P + min(p0 + 127, g.C - 1)) / g.bs;
+  const int jfull = (g.P + p0 + 1) / g.bs - 1;  // last block with j*bs + bs - 1 <= P + p0
+  if (args.indptr == nullptr) {
+    *start = 0;
+    *n = jmax + 1;
+    *nd = min(jfull + 1, jmax + 1);
+    return;
+  }
+  const int r = c.b * g.Gn + c.grp;
+  const int s = args.indptr[r];
+  int lo = s, hi = args.indptr[r + 1];  // first index with kv_indices > jmax
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (args.indices[mid] <= jmax) lo = mid + 1; else hi = mid;
+  }
+  const int e = lo;
+  lo = s;
+  hi = e;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (args.indices[mid] <= jfull) lo = mid + 1; else hi = mid;
+  }
+  *start = s;
+  *n = e - s;
+  *nd = lo - s;
+}
+
+// Page range [lo, hi) of persistent cluster c in segment s (a segment = the units of one (b, group)
+// row; every cluster takes the c-th equal share of every segment, segment after segment, so all
+// clusters read the same group's KV pages at the same time, as in the per-unit grid).
+__device__ __forceinline__ void sk_range(const SkSched& sk, int c, int s, int* lo, int* hi) {
+  const int b0 = sk.pre[s * sk.seg_units], b1 = sk.pre[(s + 1) * sk.seg_units];
+  const long long T = b1 - b0;
+  *lo = b0 + (int)(T * c / sk.clusters);
+  *hi = b0 + (int)(T * (c + 1) / sk.clusters);
+}
+// Unit containing global page x (last u with pre[u] <= x).
+__device__ __forceinline__ int sk_unit_of(const SkSched& sk, int x) {
+  int lo = 0, hi = sk.units;  // first u with pre[u] > x, minus one
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sk.pre[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo - 1;
+}
+
+// Stream-K schedule (one CTA): per unit its table start / length / fully-visible prefix, and the
+// exclusive prefix sum of the lengths (sched->pre[U] = total pages).
+__global__ void __launch_bounds__(1024) k_sk_schedule(Geo g, AttnArgs args, SkSched sk) {
+  __shared__ int part[1024];
+  const int U = sk.units, tid = threadIdx.x;
+  const int per = (U + 1023) / 1024;
+  const int u0 = min(U, tid * per), u1 = min(U, u0 + per);
+  int sum = 0;
+  for (int u = u0; u < u1; ++u) {
+    int s, n, nd;
+    unit_table(g, args, u, &s, &n, &nd);
+    sk.start[u] = s;
+    sk.len[u] = n;
+    sk.nd[u] = nd;
+    sum += n;
+  }
+  part[tid] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan of the per-thread sums
+    const int v = tid >= off ? part[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = part[tid] - sum;
+  for (int u = u0; u < u1; ++u) {
+    sk.pre[u] = run;
+    run += sk.len[u];
+  }
+  if (tid == 1023) sk.pre[U] = part[1023];
+  __syncthreads();
+  // fixup part lists, one share (c, s) per thread: the share that holds a unit's FIRST page and not
+  // its last owns the merge; its parts are its own item of that unit (slot 0 if it is the share's
+  // first item, else 1) and the first item (slot 0) of every later non-empty share up to the one
+  // holding the unit's last page
+  for (int cs = tid; cs < sk.clusters * sk.segments; cs += 1024) {
+    const int c = cs % sk.clusters, sg = cs / sk.clusters;
+    int* fx = sk.fix + (long long)cs * kSkFixStride;
+    fx[0] = 0;
+    int lo, hi;
+    sk_range(sk, c, sg, &lo, &hi);
+    if (lo >= hi) continue;
+    const int u = sk_unit_of(sk, hi - 1);
+    const int base = sk.pre[u], len = sk.len[u];
+    if (base < lo || base + len <= hi) continue;
+    int n = 0;
+    fx[2 + n++] = (c * sk.segments + sg) * 2 + (sk_unit_of(sk, lo) == u ? 0 : 1);
+    const int x = base + len - 1;
+    for (int cc = c + 1; cc < sk.clusters && n < kSkFixStride - 2; ++cc) {
+      int l2, h2;
+      sk_range(sk, cc, sg, &l2, &h2);
+      if (l2 > x) break;
+      if (l2 < h2) fx[2 + n++] = (cc * sk.segments + sg) * 2;
+    }
+    fx[1] = u;
+    fx[0] = n;
+  }
+}
+
+// Walks the items (unit, page range [a, e) of the unit's list) of one cluster, in order. Every role
+// of the cluster runs its own cursor over the same deterministic sequence. Non-persistent: the one
+// item of the prologue (whole unit); persistent: the units overlapping the cluster's page range.
+struct ItemCursor {
+  int idx, u, a, e, start, nd, len;
+  int cur, hi, seg, c;
+  bool valid, first_in_seg;
+  __device__ __forceinline__ void load(const SkSched& sk) {  // unit u, from page cur (next segments if done)
+    for (;;) {
+      if (cur >= hi) {
+        if (++seg >= sk.segments) break;
+        sk_range(sk, c, seg, &cur, &hi);
+        u = sk_unit_of(sk, cur);
+        first_in_seg = true;
+        continue;
+      }
+      const int base = sk.pre[u];
+      len = sk.len[u];
+      a = cur - base;
+      e = min(hi - base, len);
+      if (e > a) {
+        start = sk.start[u];
+        nd = sk.nd[u];
+        valid = true;
+        return;
+      }
+      cur = base + len;
+      ++u;
+    }
+    valid = false;
+  }
+  __device__ __forceinline__ void init(const SkSched& sk, int c, const int* single) {
+    idx = 0;
+    if (sk.pre == nullptr) {  // single[] = {unit, start, n, nd}
+      u = single[0]; start = single[1]; len = single[2]; nd = single[3];
+      a = 0; e = len; valid = len > 0; cur = hi = 0;
+      return;
+    }
+    this->c = c;
+    seg = 0;
+    sk_range(sk, c, 0, &cur, &hi);
+    u = sk_unit_of(sk, cur);
+    first_in_seg = true;
+    load(sk);
+  }
+  __device__ __forceinline__ void next(const SkSched& sk) {
+    ++idx;
+    if (sk.pre == nullptr) { valid = false; return; }
+    cur = sk.pre[u] + e;
+    ++u;
+    first_in_seg = false;
+    load(sk);
+  }
+  // partial-output slot of the current item (only a segment range's first / last item can be cut)
+  __device__ __forceinline__ int slot(const SkSched& sk) const {
+    return (c * sk.segments + seg) * 2 + (first_in_seg ? 0 : 1);
+  }
 };
 
 template <int BS, bool PF16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     k_paged_attn_2cta(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k_half,
-                      const __grid_constant__ CUtensorMap tm_v, Geo g, AttnArgs args) {
+                      const __grid_constant__ CUtensorMap tm_v, Geo g, AttnArgs args, SkSched sk) {
   using Cfg = Attn2Cfg<BS>;
   constexpr int D = Cfg::D;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Cfg::kQBytes;
+  uint8_t* sQ = smem;                                   // [2] Q buffers (item parity)
+  uint8_t* sK = sQ + 2 * Cfg::kQBytes;
   uint8_t* sV = sK + Cfg::kKStages * Cfg::kKHalf;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::kVStages * Cfg::kVHalf);
-  uint64_t* q_full = bars;                          // leader: both Q tiles landed (tx)
-  uint64_t* k_full = q_full + 1;                    // leader: both K halves landed (tx)
+  uint64_t* q_full = bars;                          // leader [2]: both Q tiles of buffer q landed (tx)
+  uint64_t* q_empty = q_full + 2;                   // both [2]: last S of the buffer's item done (multicast)
+  uint64_t* k_full = q_empty + 2;                   // leader: both K halves landed (tx)
   uint64_t* k_empty = k_full + Cfg::kKStages;       // both: K stage consumed (multicast commit)
   uint64_t* v_full = k_empty + Cfg::kKStages;       // local: own V half landed (tx)
   uint64_t* v_empty = v_full + Cfg::kVStages;       // both: V stage consumed (multicast commit)
@@ -70,28 +264,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* s_full = v_ready + Cfg::kVStages;       // both [2]: S^b computed (multicast commit)
   uint64_t* p_full = s_full + 2;                    // leader [2][2]: P^b columns of WG w written
   uint64_t* pv_done = p_full + 4;                   // both [2]: last P.V into O_w complete
-  uint64_t* o_full = pv_done + 2;                   // both: every MMA complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 1);
-  int* n_blocks_s = reinterpret_cast<int*>(tmem_slot + 1);
-  int* row_start_s = n_blocks_s + 1;
-  int* n_diag_s = row_start_s + 1;
+  uint64_t* o_full = pv_done + 2;                   // both: every MMA of the item complete
+  uint64_t* o_empty = o_full + 1;                   // leader: epilogue read O (16 warp arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  int* total_s = reinterpret_cast<int*>(tmem_slot + 1);
+  int* single_s = total_s + 1;  // non-persistent unit: {unit, start, n, nd}
 
   const uint32_t cta = cluster_ctarank();
   const bool leader = cta == 0;
-  // ---- tile coordinates; one cluster = one (b, g, q-tile, head pair). Execution-group-major order
-  // (heaviest q-tile first within a group) so the clusters in flight share few groups' KV pages in L2.
   const int cl = (int)blockIdx.x >> 1;
-  const int HP = g.E / 2;
-  const int nqt = (g.C + 127) / 128;
-  const int hp = cl % HP;
-  const int qt = nqt - 1 - (cl / HP) % nqt;
-  const int bg = cl / (HP * nqt);
-  const int grp = bg % g.Gn;
-  const int b = bg / g.Gn;
-  const int p0 = qt * 128;
-  const int h = grp * g.E + hp * 2 + (int)cta;  // this CTA's query head
-  const int kvh = group_kv_head(g, grp);
-
   const uint32_t warp = warp_id(), lane = lane_id();
   constexpr uint32_t kConvWarp0 = 8, kTmaWarp = 10, kMmaWarp = 11;
 
@@ -99,7 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_k_half);
     tma_prefetch_desc(&tm_v);
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
     for (int s = 0; s < Cfg::kKStages; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
     for (int s = 0; s < Cfg::kVStages; ++s) {
       mbar_init(v_full + s, 1);
@@ -112,98 +293,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(pv_done, 1);
     mbar_init(pv_done + 1, 1);
     mbar_init(o_full, 1);
+    mbar_init(o_empty, 16);  // 8 softmax warps x 2 CTAs
     fence_barrier_init();
-    const int last_abs = g.P + min(p0 + 127, g.C - 1);
-    const int jmax = last_abs / g.bs;
-    const int r = b * g.Gn + grp;
-    int start = 0, n = jmax + 1;
-    if (args.indptr != nullptr) {
-      start = args.indptr[r];
-      int lo = start, hi = args.indptr[r + 1];  // first index with kv_indices > jmax
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (args.indices[mid] <= jmax) lo = mid + 1; else hi = mid;
+    if (sk.pre == nullptr) {  // one cluster = one whole unit
+      int s, n, nd;
+      unit_table(g, args, cl, &s, &n, &nd);
+      single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd;
+      *total_s = n;
+    } else {  // stream-K: share cl of every segment
+      int total = 0;
+      for (int s = 0; s < sk.segments; ++s) {
+        int lo, hi;
+        sk_range(sk, cl, s, &lo, &hi);
+        total += hi - lo;
       }
-      n = lo - start;
+      *total_s = total;
     }
-    // table entries before n_diag are fully visible to every row of the tile (no causal mask)
-    const int jfull = (g.P + p0 + 1) / g.bs - 1;  // last block with j*bs + bs - 1 <= P + p0
-    int nd = jfull + 1;
-    if (args.indptr != nullptr) {
-      int lo = start, hi = start + n;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (args.indices[mid] <= jfull) lo = mid + 1; else hi = mid;
-      }
-      nd = lo - start;
-    }
-    *n_blocks_s = n;
-    *row_start_s = start;
-    *n_diag_s = min(nd, n);
   }
   if (warp == kMmaWarp) tmem_alloc2<512>(tmem_slot);
   tc_fence_before();
   cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int N = *n_blocks_s;
-  const int row_start = *row_start_s;
-  const int n_diag = *n_diag_s;
+  const int G = *total_s;  // pages this cluster processes (all items)
 
   if (warp == kTmaWarp) {
-    if (N > 0) {  // ------------------------------------------------------------ TMA producer
-      if (elect_one()) {
-        if (leader) mbar_expect_tx(q_full, 2 * Cfg::kQBytes);
-        tma_load_4d_2sm(sQ, &tm_q, q_full, 0, h, p0, b);
-        tma_load_4d_2sm(sQ + 128 * 128, &tm_q, q_full, 64, h, p0, b);
-      }
-      __syncwarp();
-      const int32_t* ptab = args.page_table + (long long)b * g.maxb;
-      for (int n = 0; n < N; ++n) {
-        const int j = args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
-        const int page = __ldg(ptab + j);
-        const int ks = n % Cfg::kKStages, vs = n % Cfg::kVStages;
-        mbar_wait(k_empty + ks, ((n / Cfg::kKStages) & 1) ^ 1);
+    if (G > 0) {  // ------------------------------------------------------------ TMA producer
+      int n = 0;
+      ItemCursor it;
+      for (it.init(sk, cl, single_s); it.valid; it.next(sk)) {
+        const int i = it.idx;
+        const Unit uc = unit_coords(g, it.u);
+        const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;
+        const int kvh = group_kv_head(g, uc.grp);
+        const int qb = i & 1;
+        mbar_wait(q_empty + qb, ((i >> 1) & 1) ^ 1);
         if (elect_one()) {
-          if (leader) mbar_expect_tx(k_full + ks, 2 * Cfg::kKHalf);
-          uint8_t* dst = sK + ks * Cfg::kKHalf;
-          tma_load_4d_2sm(dst, &tm_k_half, k_full + ks, 0, (int)cta * (BS / 2), kvh, page);
-          tma_load_4d_2sm(dst + (BS / 2) * 128, &tm_k_half, k_full + ks, 64, (int)cta * (BS / 2), kvh, page);
+          if (leader) mbar_expect_tx(q_full + qb, 2 * Cfg::kQBytes);
+          uint8_t* dq = sQ + qb * Cfg::kQBytes;
+          tma_load_4d_2sm(dq, &tm_q, q_full + qb, 0, h, uc.qt * 128, uc.b);
+          tma_load_4d_2sm(dq + 128 * 128, &tm_q, q_full + qb, 64, h, uc.qt * 128, uc.b);
         }
         __syncwarp();
-        mbar_wait(v_empty + vs, ((n / Cfg::kVStages) & 1) ^ 1);
-        if (elect_one()) {
-          mbar_expect_tx(v_full + vs, Cfg::kVHalf);
-          tma_load_4d(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+        const int32_t* ptab = args.page_table + (long long)uc.b * g.maxb;
+        const int st = it.start;
+        for (int t = it.a; t < it.e; ++t, ++n) {
+          const int j = args.indptr != nullptr ? __ldg(args.indices + st + t) : t;
+          const int page = __ldg(ptab + j);
+          const int ks = n % Cfg::kKStages, vs = n % Cfg::kVStages;
+          mbar_wait(k_empty + ks, ((n / Cfg::kKStages) & 1) ^ 1);
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(k_full + ks, 2 * Cfg::kKHalf);
+            uint8_t* dst = sK + ks * Cfg::kKHalf;
+            tma_load_4d_2sm(dst, &tm_k_half, k_full + ks, 0, (int)cta * (BS / 2), kvh, page);
+            tma_load_4d_2sm(dst + (BS / 2) * 128, &tm_k_half, k_full + ks, 64, (int)cta * (BS / 2), kvh, page);
+          }
+          __syncwarp();
+          mbar_wait(v_empty + vs, ((n / Cfg::kVStages) & 1) ^ 1);
+          if (elect_one()) {
+            mbar_expect_tx(v_full + vs, Cfg::kVHalf);
+            tma_load_4d(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
     }
   } else if (warp == kMmaWarp) {
-    if (leader && N > 0) {  // ---------------------------------------------------- MMA issuer (CTA 0)
+    if (leader && G > 0) {  // ---------------------------------------------------- MMA issuer (CTA 0)
       constexpr uint32_t idesc_s = umma_idesc_bf16(256, BS, 0, 0);
       constexpr uint32_t idesc_o = umma_idesc_bf16(256, D, 0, 1) & ~(PF16 ? ((7u << 7) | (7u << 10)) : 0u);
       const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
-      auto issue_s = [&](int n) {  // S^{n%2} = Q K_n^T, M=256 (both CTAs' rows), N=BS, K=d
+      // item cursor of the S issue (runs 2 pages ahead of the P.V issue)
+      ItemCursor si;
+      si.init(sk, cl, single_s);
+      int s_left = si.e - si.a;
+      auto issue_s = [&](int n) {  // S^{n%2} = Q_item K_n^T, M=256 (both CTAs' rows), N=BS, K=d
+        const int s_item = si.idx;
+        const bool first = s_left == si.e - si.a;
+        if (first) {
+          mbar_wait(q_full + (s_item & 1), (s_item >> 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t qb = q_base + (s_item & 1) * Cfg::kQBytes;
         const uint32_t d_tm = tmem + (n & 1) * 128;
         const uint32_t kb = k_base + (n % Cfg::kKStages) * Cfg::kKHalf;
+        const bool last = s_left == 1;
         if (elect_one()) {
 #pragma unroll
           for (int a = 0; a < 2; ++a)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t ad = umma_desc_sw128(q_base + a * 128 * 128 + kk * 32, 16, 1024);
+              const uint64_t ad = umma_desc_sw128(qb + a * 128 * 128 + kk * 32, 16, 1024);
               const uint64_t bd = umma_desc_sw128(kb + a * (BS / 2) * 128 + kk * 32, 16, 1024);
               mma2_ss(d_tm, ad, bd, idesc_s, (a | kk) != 0);
             }
           tc_commit2(s_full + (n & 1));
           tc_commit2(k_empty + n % Cfg::kKStages);
+          if (last) tc_commit2(q_empty + (s_item & 1));
         }
         __syncwarp();
+        if (last) {
+          si.next(sk);
+          if (si.valid) s_left = si.e - si.a;
+        } else {
+          --s_left;
+        }
       };
       // O_w += P_w V_n[w-half keys]: WG w's P (keys [w BS/2, (w+1) BS/2) of page n, fp16 packed over its
       // S^b columns) times those V rows; M=256, N=d (64 cols per CTA), K=BS/2
-      auto issue_pv = [&](int n, int w) {
+      auto issue_pv = [&](int n, int w, bool first, bool last) {
         const uint32_t p_tm = tmem + (n & 1) * 128 + w * (BS / 2);
         const uint32_t o_tm = tmem + 256 + w * 128;
         const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kVHalf + w * (BS / 2) * 128;
@@ -211,10 +409,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #pragma unroll
           for (int kk = 0; kk < BS / 32; ++kk) {
             const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
-            mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (n > 0 || kk > 0) ? 1u : 0u);
+            mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
           }
           tc_commit2(pv_done + w);
-          if (w == 1) tc_commit2(v_empty + n % Cfg::kVStages);
+          if (w == 1) {
+            tc_commit2(v_empty + n % Cfg::kVStages);
+            if (last) tc_commit2(o_full);
+          }
         }
         __syncwarp();
       };
@@ -222,36 +423,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         mbar_wait(k_full + n % Cfg::kKStages, (n / Cfg::kKStages) & 1);
         tc_fence_after();
       };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      for (int n = 0; n < 2 && n < N; ++n) {
+      for (int n = 0; n < 2 && n < G; ++n) {
         wait_k(n);
         issue_s(n);
       }
-      for (int n = 0; n < N; ++n) {
-        mbar_wait(v_ready + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
-        if (lane == 0) TRACE2(1, n);
-        mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
-        if (lane == 0) TRACE2(2, n);
-        tc_fence_after();
-        issue_pv(n, 0);
-        mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
-        tc_fence_after();
-        issue_pv(n, 1);
-        if (lane == 0) TRACE2(9, n);
-        if (n + 2 < N) {
-          wait_k(n + 2);
-          if (lane == 0) TRACE2(10, n);
-          issue_s(n + 2);
+      int n = 0;
+      ItemCursor it;
+      for (it.init(sk, cl, single_s); it.valid; it.next(sk)) {
+        const int i = it.idx;
+        for (int t = it.a; t < it.e; ++t, ++n) {
+          const bool first = t == it.a, last = t + 1 == it.e;
+          mbar_wait(v_ready + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
+          if (lane == 0) TRACE2(1, n);
+          if (first && i > 0) mbar_wait(o_empty, (i - 1) & 1);  // previous item's O read out of TMEM
+          mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
+          if (lane == 0) TRACE2(2, n);
+          tc_fence_after();
+          issue_pv(n, 0, first, last);
+          mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+          tc_fence_after();
+          issue_pv(n, 1, first, last);
+          if (lane == 0) TRACE2(9, n);
+          if (n + 2 < G) {
+            wait_k(n + 2);
+            if (lane == 0) TRACE2(10, n);
+            issue_s(n + 2);
+          }
+          if (lane == 0) TRACE2(3, n);
         }
-        if (lane == 0) TRACE2(3, n);
       }
-      if (elect_one()) tc_commit2(o_full);
-      __syncwarp();
     }
   } else if (warp >= kConvWarp0) {  // --------------------------------------- V bf16 -> fp16
     const int ct = (warp - kConvWarp0) * 32 + lane;
-    for (int n = 0; n < N; ++n) {
+    for (int n = 0; n < G; ++n) {
       const int vs = n % Cfg::kVStages;
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
       if (ct == 0) TRACE2(7, n);
@@ -284,133 +488,164 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     __shared__ float xml[2][2][128];  // [WG][m, l][row] for the final merge
     const int wg = warp >> 2, quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    const int p = p0 + row;
-    const int lim = min(g.P + p, g.L - 1);
     const float sl2 = g.scale * 1.4426950408889634f;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     constexpr int HC = BS / 2;                                // key columns of a page per WG
     const uint32_t s_tm0 = tmem + lane_off + wg * HC;         // WG's columns of S^0 (this row's lanes)
     const uint32_t o_tm = tmem + lane_off + 256 + wg * 128;  // O_wg
-    float m_run = -INFINITY, l_run = 0.f;
-    // Both WGs work on every page: WG w owns key columns [w BS/2, (w+1) BS/2) of each S^b with its own
-    // running max / sum and its own accumulator O_w (no cross-WG exchange until the epilogue merge).
-    for (int n = 0; n < N; ++n) {
-      const uint32_t s_tm = s_tm0 + (n & 1) * 128;
-      if (row == 0) TRACE2(4 + 16 * wg, n);
-      mbar_wait(s_full + (n & 1), (n >> 1) & 1);
-      if (row == 0) TRACE2(5 + 16 * wg, n);
-      tc_fence_after();
+    int n = 0;
+    ItemCursor it;
+    for (it.init(sk, cl, single_s); it.valid; it.next(sk)) {
+      const int i = it.idx;
+      const Unit uc = unit_coords(g, it.u);
+      const int p0 = uc.qt * 128;
+      const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;  // this CTA's query head
+      const int p = p0 + row;
+      const int lim = min(g.P + p, g.L - 1);
+      const int st = it.start, nd = it.nd, ta = it.a, te = it.e;
+      float m_run = -INFINITY, l_run = 0.f;
+      // Both WGs work on every page: WG w owns key columns [w BS/2, (w+1) BS/2) of each S^b with its
+      // own running max / sum and its own accumulator O_w (no cross-WG exchange until the merge).
+      for (int t = ta; t < te; ++t, ++n) {
+        const uint32_t s_tm = s_tm0 + (n & 1) * 128;
+        if (row == 0) TRACE2(4 + 16 * wg, n);
+        mbar_wait(s_full + (n & 1), (n >> 1) & 1);
+        if (row == 0) TRACE2(5 + 16 * wg, n);
+        tc_fence_after();
 #ifdef CPA_EXP_NO_SOFTMAX  // A/B only: MMA / TMA / converter pipeline alone (wrong results)
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
-      continue;
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
+        continue;
 #endif
-      uint32_t sv[HC / 32][32];
+        uint32_t sv[HC / 32][32];
 #pragma unroll
-      for (int k = 0; k < HC / 32; ++k) tmem_ld32(s_tm + k * 32, sv[k]);
-      tmem_wait_ld();
-      if (n >= n_diag) {  // block crosses the causal diagonal of this tile: mask in absolute positions
-        const int j = args.indptr != nullptr ? __ldg(args.indices + row_start + n) : n;
-        const int tbase = j * g.bs + wg * HC;
+        for (int k = 0; k < HC / 32; ++k) tmem_ld32(s_tm + k * 32, sv[k]);
+        tmem_wait_ld();
+        if (t >= nd) {  // block crosses the causal diagonal of this tile: mask in absolute positions
+          const int j = args.indptr != nullptr ? __ldg(args.indices + st + t) : t;
+          const int tbase = j * g.bs + wg * HC;
+#pragma unroll
+          for (int k = 0; k < HC / 32; ++k)
+#pragma unroll
+            for (int c = 0; c < 32; ++c)
+              if (tbase + k * 32 + c > lim) sv[k][c] = __float_as_uint(-INFINITY);
+        }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int k = 0; k < HC / 32; ++k)
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (tbase + k * 32 + c > lim) sv[k][c] = __float_as_uint(-INFINITY);
-      }
-      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+          for (int c = 0; c < 32; c += 8)
 #pragma unroll
-      for (int k = 0; k < HC / 32; ++k)
+            for (int w4 = 0; w4 < 4; ++w4)
+              m4[w4] = fmax3(m4[w4], __uint_as_float(sv[k][c + 2 * w4]), __uint_as_float(sv[k][c + 2 * w4 + 1]));
+        const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
+        float f = 1.f;
+        const bool rescale = m_blk > m_run + 8.0f;  // lazy rescale (first block always lands here)
+        if (rescale) {
+          if (m_run != -INFINITY) f = fast_exp2(m_run - m_blk);
+          m_run = m_blk;
+        }
+        const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
+        if (row == 0) TRACE2(11 + 16 * wg, n);
+        // P = exp2(s*sl2 - m): packed f32x2 FFMA; pairs chosen by use_poly_exp on a degree-3
+        // polynomial (FMA pipe), the rest on MUFU.EX2; 4 partial f32x2 sums; fp16 pack; stored over S.
+        float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
-        for (int c = 0; c < 32; c += 8)
+        for (int k = 0; k < HC / 32; ++k) {
+          uint32_t pk[16];
 #pragma unroll
-          for (int w4 = 0; w4 < 4; ++w4)
-            m4[w4] = fmax3(m4[w4], __uint_as_float(sv[k][c + 2 * w4]), __uint_as_float(sv[k][c + 2 * w4 + 1]));
-      const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
-      float f = 1.f;
-      const bool rescale = m_blk > m_run + 8.0f;  // lazy rescale (first block always lands here)
-      if (rescale) {
-        if (m_run != -INFINITY) f = fast_exp2(m_run - m_blk);
-        m_run = m_blk;
-      }
-      const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
-      if (row == 0) TRACE2(11 + 16 * wg, n);
-      // P = exp2(s*sl2 - m): packed f32x2 FFMA; pairs chosen by use_poly_exp on a degree-3
-      // polynomial (FMA pipe), the rest on MUFU.EX2; 4 partial f32x2 sums; fp16 pack; stored over S.
-      float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll
-      for (int k = 0; k < HC / 32; ++k) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int q2 = 0; q2 < 16; ++q2) {
-          float2 x = ffma2(make_float2(__uint_as_float(sv[k][2 * q2]), __uint_as_float(sv[k][2 * q2 + 1])), sl2, -m_use);
-          float2 e;
-          if (PF16 && use_poly_exp(q2)) {
-            e = exp2_poly2(x);
-          } else {
-            e.x = fast_exp2(x.x);
-            e.y = fast_exp2(x.y);
+          for (int q2 = 0; q2 < 16; ++q2) {
+            float2 x = ffma2(make_float2(__uint_as_float(sv[k][2 * q2]), __uint_as_float(sv[k][2 * q2 + 1])), sl2, -m_use);
+            float2 e;
+            if (PF16 && use_poly_exp(q2)) {
+              e = exp2_poly2(x);
+            } else {
+              e.x = fast_exp2(x.x);
+              e.y = fast_exp2(x.y);
+            }
+            acc[q2 & 3] = fadd2(acc[q2 & 3], e);
+            pk[q2] = PF16 ? pack_f16x2(e.x, e.y) : pack_bf16x2(e.x, e.y);
           }
-          acc[q2 & 3] = fadd2(acc[q2 & 3], e);
-          pk[q2] = PF16 ? pack_f16x2(e.x, e.y) : pack_bf16x2(e.x, e.y);
+          tmem_st16(s_tm + k * 16, pk);
         }
-        tmem_st16(s_tm + k * 16, pk);
-      }
-      const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-      l_run = l_run * f + ((a01.x + a01.y) + (a23.x + a23.y));
-      if (row == 0) TRACE2(12 + 16 * wg, n);
-      // rescale O_wg (own rows) after this WG's previous P.V completed, before PV_wg(n) is issued
-      if (__any_sync(0xffffffffu, rescale && n > 0)) {
-        mbar_wait(pv_done + wg, (n - 1) & 1);
-        tc_fence_after();
+        const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+        l_run = l_run * f + ((a01.x + a01.y) + (a23.x + a23.y));
+        if (row == 0) TRACE2(12 + 16 * wg, n);
+        // rescale O_wg (own rows) after this WG's previous P.V completed, before PV_wg(n) is issued;
+        // not on an item's first page (its P.V overwrites O)
+        if (__any_sync(0xffffffffu, rescale && t > ta)) {
+          mbar_wait(pv_done + wg, (n - 1) & 1);
+          tc_fence_after();
 #pragma unroll 1
-        for (int c0 = 0; c0 < D; c0 += 32) {
-          uint32_t o[32];
-          tmem_ld32(o_tm + c0, o);
-          tmem_wait_ld();
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t o[32];
+            tmem_ld32(o_tm + c0, o);
+            tmem_wait_ld();
 #pragma unroll
-          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-          tmem_st16(o_tm + c0, *reinterpret_cast<uint32_t(*)[16]>(o));
-          tmem_st16(o_tm + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(o + 16));
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            tmem_st16(o_tm + c0, *reinterpret_cast<uint32_t(*)[16]>(o));
+            tmem_st16(o_tm + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(o + 16));
+          }
         }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
+        if (row == 0) TRACE2(6 + 16 * wg, n);
       }
-      tmem_wait_st();
+      // ---- item epilogue: merge the two half-softmaxes, O = (O_0 a_0 + O_1 a_1) / (l_0 a_0 + l_1 a_1),
+      // a_w = 2^(m_w - m); WG w stores output columns [64w, 64w+64). A unit cut by a stream-K range
+      // boundary is stored unnormalised with (m, l) for k_sk_fixup.
+      xml[wg][0][row] = m_run;
+      xml[wg][1][row] = l_run;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // warps q and q+4
+      const float m0 = xml[0][0][row], l0 = xml[0][1][row], m1 = xml[1][0][row], l1 = xml[1][1][row];
+      const float mm = fmaxf(m0, m1);
+      const float a0 = l0 > 0.f ? fast_exp2(m0 - mm) : 0.f, a1 = l1 > 0.f ? fast_exp2(m1 - mm) : 0.f;
+      const float lt = l0 * a0 + l1 * a1;
+      const bool partial = ta > 0 || te < it.len;
+      // a row with no visible key in this item (possible only in a stream-K share made of pages past
+      // the row's diagonal) contributes nothing: (m, l, O) = (-inf, 0, 0). (Its m is -inf but l is a
+      // tiny positive sum of the polynomial exp2's clamped 2^-126 terms, so a_w = 2^(m_w - mm) is NaN.)
+      const bool empty_row = !(lt > 0.f);
+      const float inv = partial ? 1.f : (lt > 0.f ? 1.0f / lt : 0.f);
+      const float c0f = a0 * inv, c1f = a1 * inv;
+      mbar_wait(o_full, i & 1);
+      tc_fence_after();
+      const uint32_t ob0 = tmem + lane_off + 256 + wg * (D / 2), ob1 = ob0 + 128;
+      float vv[D / 2];
+#pragma unroll
+      for (int cc = 0; cc < D / 2; cc += 32) {
+        uint32_t o0[32], o1[32];
+        tmem_ld32(ob0 + cc, o0);
+        tmem_ld32(ob1 + cc, o1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c)
+          vv[cc + c] = empty_row ? 0.f : __uint_as_float(o0[c]) * c0f + __uint_as_float(o1[c]) * c1f;
+      }
+      // O is in registers: release TMEM to the next item's first P.V before the global stores
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
-      if (row == 0) TRACE2(6 + 16 * wg, n);
-    }
-    // ---- epilogue: merge the two half-softmaxes, O = (O_0 a_0 + O_1 a_1) / (l_0 a_0 + l_1 a_1),
-    // a_b = 2^(m_b - m); WG b normalises and stores output columns [64b, 64b+64).
-    xml[wg][0][row] = m_run;
-    xml[wg][1][row] = l_run;
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // warps q and q+4
-    const float m0 = xml[0][0][row], l0 = xml[0][1][row], m1 = xml[1][0][row], l1 = xml[1][1][row];
-    const float mm = fmaxf(m0, m1);
-    const float a0 = l0 > 0.f ? fast_exp2(m0 - mm) : 0.f, a1 = l1 > 0.f ? fast_exp2(m1 - mm) : 0.f;
-    const float lt = l0 * a0 + l1 * a1;
-    const float inv = lt > 0.f ? 1.0f / lt : 0.f;
-    const float c0f = a0 * inv, c1f = a1 * inv;
-    const bool has0 = N > 0, has1 = N > 0;  // both accumulators are written on every page
-    const bool store = p < g.C;
-    if (N > 0) {
-      mbar_wait(o_full, 0);
-      tc_fence_after();
-    }
-    const uint32_t ob0 = tmem + lane_off + 256 + wg * (D / 2), ob1 = ob0 + 128;
-    const long long obase =
-        (long long)b * args.o_bstride + (long long)p * args.o_stride + (long long)h * D + wg * (D / 2);
+      if (lane == 0) mbar_arrive_cluster(o_empty, 0);
+      if (!partial) {
+        if (p < g.C) {
+          const long long obase = (long long)uc.b * args.o_bstride + (long long)p * args.o_stride +
+                                  (long long)h * D + wg * (D / 2);
 #pragma unroll
-    for (int cc = 0; cc < D / 2; cc += 32) {
-      uint32_t o0[32], o1[32];
-      if (has0) tmem_ld32(ob0 + cc, o0);
-      if (has1) tmem_ld32(ob1 + cc, o1);
-      tmem_wait_ld();
-      float v[32];
+          for (int cc = 0; cc < D / 2; cc += 32) store_o_row32(args, obase + cc, *reinterpret_cast<float(*)[32]>(vv + cc));
+        }
+      } else {  // unnormalised partial for k_sk_fixup
+        const int slot = it.slot(sk);
+        const int prow = (int)cta * 128 + row;
+        float4* dst = reinterpret_cast<float4*>(sk.part_o + ((long long)slot * 256 + prow) * D + wg * (D / 2));
 #pragma unroll
-      for (int c = 0; c < 32; ++c)
-        v[c] = (has0 ? __uint_as_float(o0[c]) * c0f : 0.f) + (has1 ? __uint_as_float(o1[c]) * c1f : 0.f);
-      if (store) store_o_row32(args, obase + cc, v);
+        for (int c = 0; c < D / 2; c += 4) dst[c / 4] = make_float4(vv[c], vv[c + 1], vv[c + 2], vv[c + 3]);
+        if (wg == 0) {
+          sk.part_ml[((long long)slot * 256 + prow) * 2] = empty_row ? -INFINITY : mm;
+          sk.part_ml[((long long)slot * 256 + prow) * 2 + 1] = empty_row ? 0.f : lt;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -421,29 +656,124 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 }
 
+// Merge of stream-K partials. Block (c, s) owns the unit of segment s that STARTS in cluster c's
+// share and continues past it; its parts are cluster c's slot for that item and slot 0 (first item
+// of the share) of every following cluster up to the one holding the unit's last page.
+// O = sum_k O_k 2^(m_k - m) / sum_k l_k 2^(m_k - m), m = max_k m_k.
+__global__ void __launch_bounds__(256) k_sk_fixup(Geo g, AttnArgs args, SkSched sk) {
+  // block = (share cs, chunk of 8 rows): 32 blocks per share, one row per warp
+  const int chunk = blockIdx.x & 31, cs = blockIdx.x >> 5;
+  const int* fx = sk.fix + (long long)cs * kSkFixStride;
+  const int np = fx[0];
+  if (np == 0) return;
+  const int unit = fx[1];
+  const int* parts = fx + 2;
+  const Unit uc = unit_coords(g, unit);
+  const int D = g.d;
+  // thread = (row r, 4 consecutive columns): a warp per row
+  const int tx = threadIdx.x & 31;
+  {
+    const int r = chunk * 8 + (threadIdx.x >> 5);
+    const int p = uc.qt * 128 + (r & 127);
+    if (p >= g.C) return;
+    float m = -INFINITY;
+    for (int k = 0; k < np; ++k) m = fmaxf(m, sk.part_ml[((long long)parts[k] * 256 + r) * 2]);
+    float l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < np; ++k) {
+      const long long pr = (long long)parts[k] * 256 + r;
+      const float mk = sk.part_ml[pr * 2], lk = sk.part_ml[pr * 2 + 1];
+      const float w = lk > 0.f ? exp2f(mk - m) : 0.f;
+      l += lk * w;
+      const float4 o = reinterpret_cast<const float4*>(sk.part_o + pr * D)[tx];
+      acc.x += o.x * w; acc.y += o.y * w; acc.z += o.z * w; acc.w += o.w * w;
+    }
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const int h = uc.grp * g.E + uc.hp * 2 + (r >> 7);
+    const long long off = (long long)uc.b * args.o_bstride + (long long)p * args.o_stride + (long long)h * D + tx * 4;
+    const float v0 = acc.x * inv, v1 = acc.y * inv, v2 = acc.z * inv, v3 = acc.w * inv;
+    for (int k = 0; k < args.n_out; ++k) {
+      if (args.out_f32) {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(args.outs[k]) + off) = make_float4(v0, v1, v2, v3);
+      } else {
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(args.outs[k]) + off) =
+            make_uint2(pack_bf16x2(v0, v1), pack_bf16x2(v2, v3));
+      }
+    }
+  }
+}
+
 template <int BS, bool PF16>
 static cudaError_t launch_2cta_t(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
-                                 const Geo& g, const AttnArgs& a, cudaStream_t st) {
+                                 const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st, int* launches) {
   using Cfg = Attn2Cfg<BS>;
   auto kern = k_paged_attn_2cta<BS, PF16>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
   if (e != cudaSuccess) return e;
-  const int nqt = (g.C + 127) / 128;
-  const int clusters = nqt * g.B * g.Gn * (g.E / 2);
-  kern<<<2 * clusters, Cfg::kThreads, Cfg::kSmem, st>>>(tq, tk_half, tv, g, a);
+  const int units = (g.C + 127) / 128 * g.B * g.Gn * (g.E / 2);
+  SkSched none{};
+  if (sk == nullptr) {
+    ++*launches;
+    kern<<<2 * units, Cfg::kThreads, Cfg::kSmem, st>>>(tq, tk_half, tv, g, a, none);
+    return cudaGetLastError();
+  }
+  *launches += 3;
+  k_sk_schedule<<<1, 1024, 0, st>>>(g, a, *sk);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  kern<<<2 * sk->clusters, Cfg::kThreads, Cfg::kSmem, st>>>(tq, tk_half, tv, g, a, *sk);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_sk_fixup<<<sk->clusters * sk->segments * 32, 256, 0, st>>>(g, a, *sk);
   return cudaGetLastError();
 }
 
 bool attn_2cta_supported(const Geo& g) { return g.d == 128 && (g.bs == 64 || g.bs == 128) && g.E % 2 == 0; }
 
+// Co-resident clusters of the 2-CTA kernel on this device (persistent grid size), cached per device.
+int attn_2cta_max_clusters(const Geo& g) {
+  static int cached[64][2] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int which = g.bs == 128 ? 0 : 1;
+  if (dev >= 0 && dev < 64 && cached[dev][which] > 0) return cached[dev][which];
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(Attn2Cfg<128>::kThreads);
+  cfg.gridDim = dim3(2);
+  int n = 0;
+  cudaError_t e;
+  if (g.bs == 128) {
+    cudaFuncSetAttribute(k_paged_attn_2cta<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Attn2Cfg<128>::kSmem);
+    cfg.dynamicSmemBytes = Attn2Cfg<128>::kSmem;
+    e = cudaOccupancyMaxActiveClusters(&n, k_paged_attn_2cta<128, true>, &cfg);
+  } else {
+    cudaFuncSetAttribute(k_paged_attn_2cta<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Attn2Cfg<64>::kSmem);
+    cfg.dynamicSmemBytes = Attn2Cfg<64>::kSmem;
+    e = cudaOccupancyMaxActiveClusters(&n, k_paged_attn_2cta<64, true>, &cfg);
+  }
+  if (e != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    n = sms / 2;
+  }
+  if (dev >= 0 && dev < 64) cached[dev][which] = n;
+  return n;
+}
+
 cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
-                                        const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches) {
-  ++*launches;
+                                        const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st,
+                                        int* launches) {
   const bool pf16 = !(g.flags & (1u << 8));
-  if (g.bs == 128) return pf16 ? launch_2cta_t<128, true>(tq, tk_half, tv, g, a, st)
-                               : launch_2cta_t<128, false>(tq, tk_half, tv, g, a, st);
-  if (g.bs == 64) return pf16 ? launch_2cta_t<64, true>(tq, tk_half, tv, g, a, st)
-                              : launch_2cta_t<64, false>(tq, tk_half, tv, g, a, st);
+  if (g.bs == 128) return pf16 ? launch_2cta_t<128, true>(tq, tk_half, tv, g, a, sk, st, launches)
+                               : launch_2cta_t<128, false>(tq, tk_half, tv, g, a, sk, st, launches);
+  if (g.bs == 64) return pf16 ? launch_2cta_t<64, true>(tq, tk_half, tv, g, a, sk, st, launches)
+                              : launch_2cta_t<64, false>(tq, tk_half, tv, g, a, sk, st, launches);
   return cudaErrorInvalidValue;
 }
 

@@ -44,6 +44,26 @@ struct AttnArgs {
   void* outs[kMaxOut];
 };
 
+// Stream-K schedule of the persistent 2-CTA attention (attention_2cta.cu), in the call's workspace.
+// Unit u = (b, group, q-tile, head pair) in the non-persistent cluster order; its visible table
+// prefix is entries [start[u], start[u] + len[u]) of kv_indices, the first nd[u] of them fully
+// visible; pre[] = exclusive prefix sum of len (pre[units] = total pages). Segment s = the seg_units
+// units of one (b, group) row; cluster c processes the c-th of `clusters` equal page shares of every
+// segment, in segment order. A unit cut by a share boundary leaves partials in
+// part_o [clusters][segments][2][256][d] fp32 / part_ml [...][256][2] (slot 0: the share's first
+// item, slot 1: its last).
+struct SkSched {
+  int* pre;
+  int* len;
+  int* start;
+  int* nd;
+  float* part_o;
+  float* part_ml;
+  int* fix;  // per share (c, s): [0] = #parts (0: nothing to merge here), [1] = unit, [2..] part slots
+  int units, clusters, segments, seg_units;
+};
+constexpr int kSkFixStride = 2 + 80;  // ints per share in SkSched::fix (<= 80 clusters)
+
 // Arguments of the peer completion barrier (peer.cu).
 struct PeerSig {
   uint32_t* pads[kMaxOut];  // pads[w]: rank w's signal pad u32[W], mapped into this process

@@ -341,7 +341,7 @@ def test_copy_ablation_matches_zero_copy(d, bs, B):
     ip, ix = O.tables_from_mask(M, case.E, pb)
     t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
     p = case.params
-    p.flags |= cpa.F_OUT_F32
+    p.flags |= cpa.F_OUT_F32 | cpa.F_NO_PERSIST  # same grid as the copy variant's kernel: bitwise
     o1, o2 = case.out(True), case.out(True)
     cpa.paged_attention(p, case.dq, case.cache, t, o1)
     cpa.paged_attention_copy(p, case.dq, case.cache, t, o2)
@@ -361,3 +361,75 @@ def test_chunk_step_edge_lengths(C, P, bs):
     nqb, nkvb, pb, _ = O.geometry(C, P, bs)
     assert ip[-1] >= 2 * (nkvb - pb)  # chunk blocks always tabled
     assert rel_err(got, ref["O"]) <= ATOL_REL
+
+
+@pytest.mark.parametrize("cfg_name,B,kv_heads", [("llama8b_32k", 1, 1), ("llama8b_32k", 2, 2),
+                                                ("llama8b_128k", 1, 1), ("llama8b_128k", 1, 2)])
+def test_persistent_stream_k_matches_per_unit_grid(cfg_name, B, kv_heads):
+    """One rank's shard of a multi-GPU run (1-2 KV groups: 32-128 work units for 74 SM pairs) on the
+    persistent stream-K grid (forced at 32K, where the default keeps the per-unit grid) must match one cluster per unit (CPA_F_NO_PERSIST) up to the fp32
+    merge of the units cut at share boundaries, and the oracle within the parity bar (sampled rows)."""
+    import dataclasses
+    cfg = dataclasses.replace(CONFIGS[cfg_name], batch=B)
+    seed = 16839
+    E = cfg.num_q_heads // cfg.num_kv_heads
+    k, v = make_kv(cfg, seed, kv_heads=range(kv_heads))
+    q = make_q(cfg, seed, q_heads=range(kv_heads * E))
+    P, C, L = cfg.chunk_geometry()
+    case = Case(q, k, v, P, cfg.block_size, seed=seed, flags=cpa.F_OUT_F32 | cpa.F_PERSIST)
+    assert case.params.num_kv_heads == kv_heads
+    t = cpa.alloc_tables(case.params)
+    cpa.build_tables(case.params, case.dq, case.cache, t)
+    Hq = kv_heads * E
+    p_grid = cpa.make_params(B, Hq, kv_heads, cfg.head_dim, cfg.block_size, C, P,
+                             flags=cpa.F_OUT_F32 | cpa.F_NO_PERSIST)
+    for tab in (t, None):  # sparse tables and the dense baseline
+        o_sk, o_grid = case.out(f32=True), case.out(f32=True)
+        cpa.paged_attention(case.params, case.dq, case.cache, tab, o_sk)
+        cpa.paged_attention(p_grid, case.dq, case.cache, tab, o_grid)
+        torch.cuda.synchronize()
+        a, b = o_sk.cpu().numpy(), o_grid.cpu().numpy()
+        rms = float(np.sqrt(np.mean(b.astype(np.float64) ** 2)))
+        assert np.isfinite(a).all()
+        # a cut unit's parts round P to fp16 against their own running max: differences are of the
+        # order of the fp16 P rounding (measured ~2e-3 x RMS), far inside the 1e-2 parity bar
+        assert np.abs(a - b).max() <= 5e-3 * rms, np.abs(a - b).max() / rms
+    # oracle on sampled rows of the sparse step
+    ip, ix = t.kv_indptr.cpu().numpy(), t.kv_indices.cpu().numpy()
+    ix = ix[: ip[-1]]
+    o_sk = case.out(f32=True)
+    cpa.paged_attention(case.params, case.dq, case.cache, t, o_sk)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    rows = [(int(rng.integers(B)), int(rng.integers(C)), int(rng.integers(Hq))) for _ in range(48)]
+    rows += [(B - 1, C - 1, Hq - 1), (0, 0, 0), (0, 127, 1), (0, 128, 2)]
+    ref = O.paged_attention(q, k, v, P, cfg.block_size, ip, ix, E=E, rows=rows)
+    oc = o_sk.cpu().numpy().astype(np.float64)
+    got = np.stack([oc[b, p, h] for (b, p, h) in rows])
+    want = np.stack([ref[b, p, h] for (b, p, h) in rows])
+    err = np.abs(got - want).max() / np.sqrt(np.mean(want ** 2))
+    assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,bs,C,P", [
+    (1, 4, 1, 128, 128, 256),    # 1 unit of 3 pages over 74 clusters: most shares empty, one unit cut 3 ways
+    (2, 8, 2, 128, 200, 384),    # 4 segments, ragged chunk tail
+    (1, 4, 1, 64, 300, 640),     # block size 64
+    (1, 8, 1, 128, 1024, 4096),  # GQA 8 in one segment, units cut across many shares
+])
+def test_persistent_stream_k_small_shapes(B, Hq, Hkv, bs, C, P):
+    """Forced stream-K grid (CPA_F_PERSIST) on small shapes, dense and with random tables, vs the oracle:
+    empty shares, units split over many clusters, partial last q-tile and last page."""
+    q, k, v = random_qkv(B, Hq, Hkv, 128, C, P + C, seed=B * 11 + C + bs)
+    case = Case(q, k, v, P, bs, seed=3, flags=cpa.F_OUT_F32 | cpa.F_PERSIST)
+    nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+    got = _gpu_attn(case, None)
+    assert rel_err(got, O.dense_causal_attention(q, k, v, P)) <= ATOL_REL
+    M = random_block_mask(B, Hq, nqb, nkvb, 0.3, seed=bs + C)
+    for i in range(nqb):
+        M[:, :, i, pb + i + 1:] = False
+        M[:, :, i, pb:pb + i + 1] = True
+    ip, ix = O.tables_from_mask(M, case.E, pb)
+    t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
+    got = _gpu_attn(case, t)
+    assert rel_err(got, O.paged_attention(q, k, v, P, bs, ip, ix)) <= ATOL_REL

@@ -9,15 +9,17 @@ from synth.workload import CONFIGS, make_kv, make_q, page_layout, to_pool
 cfg = CONFIGS[os.environ.get("CFG", "llama8b_128k")]
 seed = 16839 + list(CONFIGS).index(cfg.name)
 P, C, L = cfg.chunk_geometry(); bs = cfg.block_size
-k, v = make_kv(cfg, seed); q = make_q(cfg, seed)
+KVH = int(os.environ.get("KVH", cfg.num_kv_heads))  # < Hkv: one rank's KV-group shard (multi-GPU per-GPU work)
+E_ = cfg.num_q_heads // cfg.num_kv_heads
+k, v = make_kv(cfg, seed, kv_heads=range(KVH)); q = make_q(cfg, seed, q_heads=range(KVH * E_))
 pt, npg = page_layout(cfg.batch, -(-L // bs), seed)
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
 cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)), torch.from_numpy(pt).cuda())
 dq = dev(q); del k, v
-p = cpa.make_params(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06)
+p = cpa.make_params(cfg.batch, KVH * E_, KVH, cfg.head_dim, bs, C, P, alpha=0.06)
 flag_sets = [int(x, 0) for x in os.environ.get("FLAGSETS", "0").split(",")]
 rounds = int(os.environ.get("ROUNDS", "5"))
-o = torch.empty(cfg.batch, C, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
+o = torch.empty(cfg.batch, C, KVH * E_, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 variants = [(pp, f) for pp in sys.argv[1:] for f in flag_sets]
 libs = {}
