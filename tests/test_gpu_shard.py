@@ -58,7 +58,8 @@ def test_sharded_equals_unsharded(cfg_name, world):
 
 
 @pytest.mark.parametrize("cfg_name,world,f32", [("tiny", 2, True), ("llama8b_32k", 2, False),
-                                                ("llama8b_32k", 4, False), ("llama8b_32k", 8, False)])
+                                                ("llama8b_32k", 4, False), ("llama8b_32k", 8, False),
+                                                ("llama8b_128k", 8, True)])
 def test_fused_peer_allgather(cfg_name, world, f32):
     """cpa_chunk_step_peer on W simulated ranks of one GPU (each rank on its own stream, its peers'
     gathered buffers and signal pads plain device tensors, so the P2P stores are local stores): every
@@ -109,4 +110,10 @@ def test_fused_peer_allgather(cfg_name, world, f32):
         assert [int(s.item()) for s in status] == [0] * world
         assert all(int(x) == epoch + 1 for pad in pads for x in pad.cpu())
         for w in range(world):
-            assert torch.equal(outs[w], o_ref), (epoch, w)
+            if cfg_name == "llama8b_128k":
+                # a 1-group shard at 128K runs the persistent stream-K grid (the unsharded step does
+                # not): equal up to the fp32 merge of cut units
+                rms = float(o_ref.double().pow(2).mean().sqrt())
+                assert float((outs[w] - o_ref).abs().max()) <= 5e-3 * rms, (epoch, w)
+            else:
+                assert torch.equal(outs[w], o_ref), (epoch, w)
