@@ -192,8 +192,10 @@ CPA_API int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* 
  *                   (0 => W*Hq*d elements). Rank r writes heads [r*Hq, (r+1)*Hq) of every peer_out[w].
  *   peer_signal[w]: rank w's signal pad, uint32 [W], zero-initialised once before the first call.
  *                   Slot w' of rank w's pad is written only by rank w'.
- * epoch: strictly increasing across calls on the same pads (1, 2, 3, ...); the call returns (stream
- *   order) after every rank has posted `epoch`, i.e. after every peer_out[rank] is complete.
+ * epoch: 0 (default) => kept on the device: each call posts 1 + the last epoch this rank posted (read
+ *   from its own pad), so the calls stay matched across ranks and a captured CUDA graph of the step
+ *   replays correctly; nonzero => that epoch, strictly increasing across calls. The call returns
+ *   (stream order) after every rank has posted the epoch, i.e. after every peer_out[rank] is complete.
  * Reuse: a rank must not read its peer_out buffer for call k+1's purposes before that call's barrier,
  *   and must have finished reading call k's contents before ANY rank starts call k+1 (alternate two
  *   buffer sets, or call cpa_peer_barrier with a fresh epoch first).
@@ -206,7 +208,7 @@ typedef struct {
   void* const* peer_out;          /* HOST array [W] of device pointers (see above) */
   int64_t out_token_stride;       /* elements; 0 => W*Hq*d */
   uint32_t* const* peer_signal;   /* HOST array [W] of device pointers */
-  uint32_t epoch;                 /* >= 1 */
+  uint32_t epoch;                 /* 0 => device-side epochs (see above) */
   uint32_t timeout_ms;            /* 0 => 10000 */
   int32_t* dev_status;            /* optional */
 } cpa_peer_out;

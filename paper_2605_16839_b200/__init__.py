@@ -239,8 +239,8 @@ def chunk_step(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTab
 class PeerOut:
     """Peer mappings for cpa_chunk_step_peer (see cpa.h): W gathered output buffers [B, C, W*Hq, d]
     and W uint32 signal pads, given as raw device addresses valid in this process (torch symmetric
-    memory buffer_ptrs, CUDA IPC, or -- in single-GPU tests -- plain tensors on one device). The
-    epoch advances by one per call."""
+    memory buffer_ptrs, CUDA IPC, or -- in single-GPU tests -- plain tensors on one device). Epochs
+    are kept on the device (cpa.h), so a captured CUDA graph of the step can be replayed."""
 
     def __init__(self, world: int, rank: int, out_ptrs, signal_ptrs, out_token_stride: int = 0,
                  timeout_ms: int = 0, dev_status: Optional[torch.Tensor] = None):
@@ -251,8 +251,7 @@ class PeerOut:
         self.out_token_stride, self.timeout_ms, self.dev_status = out_token_stride, timeout_ms, dev_status
 
     def _next(self) -> _PeerOut:
-        self.epoch += 1
-        return _PeerOut(self.world, self.rank, self._outs, self.out_token_stride, self._sigs, self.epoch,
+        return _PeerOut(self.world, self.rank, self._outs, self.out_token_stride, self._sigs, 0,
                         self.timeout_ms, _ptr(self.dev_status))
 
 

@@ -425,7 +425,6 @@ int check_peers(const cpa_peer_out* pr) {
   if (!pr || !pr->peer_signal) return fail(CPA_ERR_NULL, "peers / peer_signal is NULL");
   if (pr->world < 1 || pr->world > CPA_MAX_PEERS || pr->rank < 0 || pr->rank >= pr->world)
     return fail(CPA_ERR_SHAPE, "world %d / rank %d out of range (world <= %d)", pr->world, pr->rank, CPA_MAX_PEERS);
-  if (pr->epoch == 0) return fail(CPA_ERR_SHAPE, "epoch must be >= 1");
   for (int w = 0; w < pr->world; ++w) {
     if (!pr->peer_signal[w]) return fail(CPA_ERR_NULL, "peer_signal[%d] is NULL", w);
     if (reinterpret_cast<uintptr_t>(pr->peer_signal[w]) & 3u) return fail(CPA_ERR_MISALIGNED, "peer_signal[%d]", w);

@@ -7,7 +7,9 @@
 // waits until every peer has told it the same, after which its own gathered buffer is complete.
 //
 // Signal pads: rank w owns u32 pad[W] (mapped into every rank); slot pad_w[r] is written only by
-// rank r, with strictly increasing epochs, so no reset is needed between calls.
+// rank r, with strictly increasing epochs, so no reset is needed between calls. The epoch is kept on
+// the device (epoch = 1 + the last one this rank posted, read from its own pad's slot r), so a
+// captured CUDA graph of the step replays with fresh epochs; a nonzero host epoch overrides it.
 #include "common.cuh"
 #include "geo.cuh"
 
@@ -31,12 +33,16 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // preceding attention kernel (same stream) are ordered before the release by the system-scope fence.
 __global__ void __launch_bounds__(32) k_peer_barrier(PeerSig s) {
   const int w = threadIdx.x;
+  uint32_t epoch = s.epoch;
+  if (epoch == 0) {  // device-side epoch: every lane reads it before lane `rank` posts the new one
+    epoch = __shfl_sync(0xffffffffu, w == 0 ? ld_acquire_sys(s.pads[s.rank] + s.rank) : 0u, 0) + 1u;
+  }
   if (w >= s.world) return;
   __threadfence_system();
-  st_release_sys(s.pads[w] + s.rank, s.epoch);
+  st_release_sys(s.pads[w] + s.rank, epoch);
   const uint32_t* mine = s.pads[s.rank] + w;
   const unsigned long long t0 = global_ns();
-  while ((int)(ld_acquire_sys(mine) - s.epoch) < 0) {
+  while ((int)(ld_acquire_sys(mine) - epoch) < 0) {
     if (global_ns() - t0 > s.timeout_ns) {  // a peer never arrived: report, do not hang the GPU
       if (s.status) atomicCAS(s.status, 0, 1 + w);
       break;

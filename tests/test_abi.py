@@ -84,7 +84,7 @@ def _peer(world, rank, outs=16, sigs=16, epoch=1, stride=0):
 
 
 @pytest.mark.parametrize("world,rank,kw,status", [
-    (0, 0, {}, 2), (9, 0, {}, 2), (2, 2, {}, 2), (2, -1, {}, 2), (2, 0, dict(epoch=0), 2),
+    (0, 0, {}, 2), (9, 0, {}, 2), (2, 2, {}, 2), (2, -1, {}, 2),
     (2, 0, dict(sigs=None), 1), (2, 0, dict(outs=None), 1), (2, 0, dict(sigs=0), 1), (2, 0, dict(sigs=18), 4),
     (2, 0, dict(outs=24), 4), (2, 0, dict(stride=100), 2),
 ])

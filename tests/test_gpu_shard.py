@@ -117,3 +117,25 @@ def test_fused_peer_allgather(cfg_name, world, f32):
                 assert float((outs[w] - o_ref).abs().max()) <= 5e-3 * rms, (epoch, w)
             else:
                 assert torch.equal(outs[w], o_ref), (epoch, w)
+    # CUDA-graph replays of every rank's step: the barrier keeps its epochs on the device
+    graphs = []
+    for p, qr, c, t, peers, st, ws in ranks:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            cpa.chunk_step_peer(p, qr, c, t, peers, workspace=ws)
+        graphs.append((g, st))
+    torch.cuda.synchronize()
+    # capture does not execute: pads still hold epoch 3
+    assert all(int(x) == 3 for pad in pads for x in pad.cpu())
+    for rep in range(2):
+        for o in outs:
+            o.fill_(float("nan"))
+        torch.cuda.synchronize()
+        for g, st in graphs:
+            with torch.cuda.stream(st):
+                g.replay()
+        torch.cuda.synchronize()
+        assert [int(s.item()) for s in status] == [0] * world
+        assert all(int(x) == 4 + rep for pad in pads for x in pad.cpu())
+        for w in range(world):
+            assert torch.isfinite(outs[w].float()).all(), (rep, w)
