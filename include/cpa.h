@@ -153,14 +153,13 @@ CPA_API int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_ca
  *   A(p) = { t : floor(t/bs) in T[b, h/E], t <= P + p }  (absolute coordinates).
  *   tables == NULL => dense causal chunk attention over every block [0, nkvb) (the baseline).
  *   o: bf16 (or fp32 with CPA_F_OUT_F32) [B, C, Hq, d], token stride p->q_token_stride.
- *   ws: >= cpa_workspace_bytes(p) (CPA_ERR_WORKSPACE otherwise). When the work units (b, group,
- *   128-token q-tile, head pair) do not fill whole waves of SM pairs and there are at most 4
- *   (b, group) rows (e.g. one rank's KV-group shard), the cta_group::2 path runs a persistent grid of
- *   one cluster per co-resident SM pair, each taking an equal contiguous share of every row's
- *   (unit, page) work, and merges units cut by a share boundary in a fixup kernel; otherwise one
- *   cluster per unit (the persistent grid is also skipped for KV shorter than 512 blocks, where the
- *   shares are too short to amortise the per-item epilogue). CPA_F_NO_PERSIST / CPA_F_PERSIST force
- *   either grid. */
+ *   ws: >= cpa_workspace_bytes(p) (CPA_ERR_WORKSPACE otherwise). The cta_group::2 path runs one
+ *   cluster per work unit (b, group, 128-token q-tile, head pair), or a persistent grid of one cluster
+ *   per co-resident SM pair, each taking an equal contiguous share of every (b, group) row's
+ *   (unit, page) work, with units cut by a share boundary merged in a fixup kernel. The persistent
+ *   grid is chosen for the dense baseline (tables == NULL) when the units do not fill whole waves,
+ *   there are at most 4 (b, group) rows and at least 512 KV blocks (measured faster there only);
+ *   CPA_F_PERSIST (at most 4 rows) / CPA_F_NO_PERSIST force either grid. */
 CPA_API int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
                         const cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
                         void* stream);

@@ -365,7 +365,10 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
     CUtensorMap tkh;  // half a page of keys per CTA of the pair
     if ((s = kv_map(&tkh, k_pages, g, num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
     const int clusters = std::min(attn_2cta_max_clusters(g), kSkMaxClusters);
-    if (ws != nullptr && !(p->flags & CPA_F_NO_PERSIST) && sk_wanted(g, clusters)) {  // persistent stream-K
+    // measured: on the sparse tables the per-unit grid is as fast (the chip is power-
+    // bound, idle SM pairs are not lost time); on the dense baseline the persistent grid is 2-5% faster
+    const bool auto_sk = indptr == nullptr && sk_wanted(g, clusters);
+    if (ws != nullptr && !(p->flags & CPA_F_NO_PERSIST) && (auto_sk || ((p->flags & CPA_F_PERSIST) && sk_wanted(g, clusters)))) {
       if (ws_bytes < attn_ws_bytes(g)) return fail(CPA_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, attn_ws_bytes(g));
       SkSched sk = carve_sk(g, ws, clusters);
       e = launch_paged_attention_2cta(tq, tkh, tv, g, a, &sk, st, &g_launches);

@@ -39,7 +39,7 @@ __device__ long long g_trace2[32][2048];
 #define TRACE2(e, i) do {} while (0)
 #endif
 
-template <int BS>
+template <int BS, bool PERSIST = false>
 struct Attn2Cfg {
   static constexpr int D = 128;
   static constexpr int kQBytes = 128 * D * 2;           // this CTA's Q tile
@@ -54,7 +54,8 @@ struct Attn2Cfg {
   static constexpr int kKStages = CPA_KSTAGES, kVStages = CPA_VSTAGES;
   static constexpr int kConvWarps = 2;
   static constexpr int kThreads = 12 * 32;       // 8 softmax + 2 converter + TMA + MMA warps
-  static constexpr int kSmem = 2 * kQBytes + kKStages * kKHalf + kVStages * kVHalf + 1024 + 512;
+  static constexpr int kQBufs = PERSIST ? 2 : 1;  // persistent: next item's Q prefetched
+  static constexpr int kSmem = kQBufs * kQBytes + kKStages * kKHalf + kVStages * kVHalf + 1024 + 512;
   static_assert(kSmem + 2048 <= 232448, "shared memory budget");
 };
 
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(1024) k_sk_schedule(Geo g, AttnArgs args, SkSc
 // Walks the items (unit, page range [a, e) of the unit's list) of one cluster, in order. Every role
 // of the cluster runs its own cursor over the same deterministic sequence. Non-persistent: the one
 // item of the prologue (whole unit); persistent: the units overlapping the cluster's page range.
+template <bool PERSIST>
 struct ItemCursor {
   int idx, u, a, e, start, nd, len;
   int cur, hi, seg, c;
@@ -216,21 +218,22 @@ struct ItemCursor {
   }
   __device__ __forceinline__ void init(const SkSched& sk, int c, const int* single) {
     idx = 0;
-    if (sk.pre == nullptr) {  // single[] = {unit, start, n, nd}
+    if constexpr (!PERSIST) {  // single[] = {unit, start, n, nd}
       u = single[0]; start = single[1]; len = single[2]; nd = single[3];
       a = 0; e = len; valid = len > 0; cur = hi = 0;
       return;
-    }
+    } else {
     this->c = c;
     seg = 0;
     sk_range(sk, c, 0, &cur, &hi);
     u = sk_unit_of(sk, cur);
     first_in_seg = true;
     load(sk);
+    }
   }
   __device__ __forceinline__ void next(const SkSched& sk) {
     ++idx;
-    if (sk.pre == nullptr) { valid = false; return; }
+    if constexpr (!PERSIST) { valid = false; return; }
     cur = sk.pre[u] + e;
     ++u;
     first_in_seg = false;
@@ -242,16 +245,17 @@ struct ItemCursor {
   }
 };
 
-template <int BS, bool PF16>
+template <int BS, bool PF16, bool PERSIST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     k_paged_attn_2cta(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k_half,
                       const __grid_constant__ CUtensorMap tm_v, Geo g, AttnArgs args, SkSched sk) {
-  using Cfg = Attn2Cfg<BS>;
+  using Cfg = Attn2Cfg<BS, PERSIST>;
+  using Cursor = ItemCursor<PERSIST>;
   constexpr int D = Cfg::D;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                                   // [2] Q buffers (item parity)
-  uint8_t* sK = sQ + 2 * Cfg::kQBytes;
+  uint8_t* sK = sQ + Cfg::kQBufs * Cfg::kQBytes;
   uint8_t* sV = sK + Cfg::kKStages * Cfg::kKHalf;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::kVStages * Cfg::kVHalf);
   uint64_t* q_full = bars;                          // leader [2]: both Q tiles of buffer q landed (tx)
@@ -295,7 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(o_full, 1);
     mbar_init(o_empty, 16);  // 8 softmax warps x 2 CTAs
     fence_barrier_init();
-    if (sk.pre == nullptr) {  // one cluster = one whole unit
+    if constexpr (!PERSIST) {  // one cluster = one whole unit
       int s, n, nd;
       unit_table(g, args, cl, &s, &n, &nd);
       single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd;
@@ -320,14 +324,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   if (warp == kTmaWarp) {
     if (G > 0) {  // ------------------------------------------------------------ TMA producer
       int n = 0;
-      ItemCursor it;
+      Cursor it;
       for (it.init(sk, cl, single_s); it.valid; it.next(sk)) {
         const int i = it.idx;
         const Unit uc = unit_coords(g, it.u);
         const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;
         const int kvh = group_kv_head(g, uc.grp);
-        const int qb = i & 1;
-        mbar_wait(q_empty + qb, ((i >> 1) & 1) ^ 1);
+        const int qb = PERSIST ? (i & 1) : 0;
+        if (PERSIST) mbar_wait(q_empty + qb, ((i >> 1) & 1) ^ 1);
         if (elect_one()) {
           if (leader) mbar_expect_tx(q_full + qb, 2 * Cfg::kQBytes);
           uint8_t* dq = sQ + qb * Cfg::kQBytes;
@@ -364,17 +368,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       constexpr uint32_t idesc_o = umma_idesc_bf16(256, D, 0, 1) & ~(PF16 ? ((7u << 7) | (7u << 10)) : 0u);
       const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
       // item cursor of the S issue (runs 2 pages ahead of the P.V issue)
-      ItemCursor si;
+      Cursor si;
       si.init(sk, cl, single_s);
       int s_left = si.e - si.a;
       auto issue_s = [&](int n) {  // S^{n%2} = Q_item K_n^T, M=256 (both CTAs' rows), N=BS, K=d
         const int s_item = si.idx;
         const bool first = s_left == si.e - si.a;
         if (first) {
-          mbar_wait(q_full + (s_item & 1), (s_item >> 1) & 1);
+          mbar_wait(q_full + (PERSIST ? (s_item & 1) : 0), PERSIST ? ((s_item >> 1) & 1) : 0);
           tc_fence_after();
         }
-        const uint32_t qb = q_base + (s_item & 1) * Cfg::kQBytes;
+        const uint32_t qb = q_base + (PERSIST ? (s_item & 1) : 0) * Cfg::kQBytes;
         const uint32_t d_tm = tmem + (n & 1) * 128;
         const uint32_t kb = k_base + (n % Cfg::kKStages) * Cfg::kKHalf;
         const bool last = s_left == 1;
@@ -389,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             }
           tc_commit2(s_full + (n & 1));
           tc_commit2(k_empty + n % Cfg::kKStages);
-          if (last) tc_commit2(q_empty + (s_item & 1));
+          if (PERSIST && last) tc_commit2(q_empty + (s_item & 1));
         }
         __syncwarp();
         if (last) {
@@ -428,14 +432,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         issue_s(n);
       }
       int n = 0;
-      ItemCursor it;
+      Cursor it;
       for (it.init(sk, cl, single_s); it.valid; it.next(sk)) {
         const int i = it.idx;
         for (int t = it.a; t < it.e; ++t, ++n) {
           const bool first = t == it.a, last = t + 1 == it.e;
           mbar_wait(v_ready + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
           if (lane == 0) TRACE2(1, n);
-          if (first && i > 0) mbar_wait(o_empty, (i - 1) & 1);  // previous item's O read out of TMEM
+          if (PERSIST && first && i > 0) mbar_wait(o_empty, (i - 1) & 1);  // previous item's O read out of TMEM
           mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
           if (lane == 0) TRACE2(2, n);
           tc_fence_after();
@@ -494,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     const uint32_t s_tm0 = tmem + lane_off + wg * HC;         // WG's columns of S^0 (this row's lanes)
     const uint32_t o_tm = tmem + lane_off + 256 + wg * 128;  // O_wg
     int n = 0;
-    ItemCursor it;
+    Cursor it;
     for (it.init(sk, cl, single_s); it.valid; it.next(sk)) {
       const int i = it.idx;
       const Unit uc = unit_coords(g, it.u);
@@ -603,7 +607,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       const float mm = fmaxf(m0, m1);
       const float a0 = l0 > 0.f ? fast_exp2(m0 - mm) : 0.f, a1 = l1 > 0.f ? fast_exp2(m1 - mm) : 0.f;
       const float lt = l0 * a0 + l1 * a1;
-      const bool partial = ta > 0 || te < it.len;
+      const bool partial = PERSIST && (ta > 0 || te < it.len);
       // a row with no visible key in this item (possible only in a stream-K share made of pages past
       // the row's diagonal) contributes nothing: (m, l, O) = (-inf, 0, 0). (Its m is -inf but l is a
       // tiny positive sum of the polynomial exp2's clamped 2^-126 terms, so a_w = 2^(m_w - mm) is NaN.)
@@ -613,35 +617,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_wait(o_full, i & 1);
       tc_fence_after();
       const uint32_t ob0 = tmem + lane_off + 256 + wg * (D / 2), ob1 = ob0 + 128;
-      float vv[D / 2];
+      // stream O from TMEM to global 32 columns at a time (final rows, or unnormalised partials)
+      const long long obase = (long long)uc.b * args.o_bstride + (long long)p * args.o_stride +
+                              (long long)h * D + wg * (D / 2);
+      const int slot = partial ? it.slot(sk) : 0;
+      const int prow = (int)cta * 128 + row;
+      float* pdst = partial ? sk.part_o + ((long long)slot * 256 + prow) * D + wg * (D / 2) : nullptr;
 #pragma unroll
       for (int cc = 0; cc < D / 2; cc += 32) {
         uint32_t o0[32], o1[32];
-        tmem_ld32(ob0 + cc, o0);
+        tmem_ld32(ob0 + cc, o0);  // warp-collective (.sync.aligned): every lane, valid row or not
         tmem_ld32(ob1 + cc, o1);
         tmem_wait_ld();
+        float v[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c)
-          vv[cc + c] = empty_row ? 0.f : __uint_as_float(o0[c]) * c0f + __uint_as_float(o1[c]) * c1f;
-      }
-      // O is in registers: release TMEM to the next item's first P.V before the global stores
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(o_empty, 0);
-      if (!partial) {
-        if (p < g.C) {
-          const long long obase = (long long)uc.b * args.o_bstride + (long long)p * args.o_stride +
-                                  (long long)h * D + wg * (D / 2);
+          v[c] = (PERSIST && empty_row) ? 0.f : __uint_as_float(o0[c]) * c0f + __uint_as_float(o1[c]) * c1f;
+        if (!partial) {
+          if (p < g.C) store_o_row32(args, obase + cc, v);
+        } else {
+          float4* dst = reinterpret_cast<float4*>(pdst + cc);
 #pragma unroll
-          for (int cc = 0; cc < D / 2; cc += 32) store_o_row32(args, obase + cc, *reinterpret_cast<float(*)[32]>(vv + cc));
+          for (int c = 0; c < 32; c += 4) dst[c / 4] = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
         }
-      } else {  // unnormalised partial for k_sk_fixup
-        const int slot = it.slot(sk);
-        const int prow = (int)cta * 128 + row;
-        float4* dst = reinterpret_cast<float4*>(sk.part_o + ((long long)slot * 256 + prow) * D + wg * (D / 2));
-#pragma unroll
-        for (int c = 0; c < D / 2; c += 4) dst[c / 4] = make_float4(vv[c], vv[c + 1], vv[c + 2], vv[c + 3]);
-        if (wg == 0) {
+      }
+      if constexpr (PERSIST) {
+        // O read out of TMEM: hand it to the next item's first P.V
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(o_empty, 0);
+        if (partial && wg == 0) {
           sk.part_ml[((long long)slot * 256 + prow) * 2] = empty_row ? -INFINITY : mm;
           sk.part_ml[((long long)slot * 256 + prow) * 2 + 1] = empty_row ? 0.f : lt;
         }
@@ -706,17 +711,22 @@ __global__ void __launch_bounds__(256) k_sk_fixup(Geo g, AttnArgs args, SkSched 
 template <int BS, bool PF16>
 static cudaError_t launch_2cta_t(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
                                  const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st, int* launches) {
-  using Cfg = Attn2Cfg<BS>;
-  auto kern = k_paged_attn_2cta<BS, PF16>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
   const int units = (g.C + 127) / 128 * g.B * g.Gn * (g.E / 2);
-  SkSched none{};
   if (sk == nullptr) {
+    using Cfg = Attn2Cfg<BS, false>;
+    auto kern = k_paged_attn_2cta<BS, PF16, false>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem)) != cudaSuccess)
+      return e;
     ++*launches;
+    SkSched none{};
     kern<<<2 * units, Cfg::kThreads, Cfg::kSmem, st>>>(tq, tk_half, tv, g, a, none);
     return cudaGetLastError();
   }
+  using Cfg = Attn2Cfg<BS, true>;
+  auto kern = k_paged_attn_2cta<BS, PF16, true>;
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem)) != cudaSuccess)
+    return e;
   *launches += 3;
   k_sk_schedule<<<1, 1024, 0, st>>>(g, a, *sk);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -743,18 +753,20 @@ int attn_2cta_max_clusters(const Geo& g) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cfg.blockDim = dim3(Attn2Cfg<128>::kThreads);
+  cfg.blockDim = dim3(Attn2Cfg<128, true>::kThreads);
   cfg.gridDim = dim3(2);
   int n = 0;
   cudaError_t e;
   if (g.bs == 128) {
-    cudaFuncSetAttribute(k_paged_attn_2cta<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Attn2Cfg<128>::kSmem);
-    cfg.dynamicSmemBytes = Attn2Cfg<128>::kSmem;
-    e = cudaOccupancyMaxActiveClusters(&n, k_paged_attn_2cta<128, true>, &cfg);
+    cudaFuncSetAttribute(k_paged_attn_2cta<128, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Attn2Cfg<128, true>::kSmem);
+    cfg.dynamicSmemBytes = Attn2Cfg<128, true>::kSmem;
+    e = cudaOccupancyMaxActiveClusters(&n, k_paged_attn_2cta<128, true, true>, &cfg);
   } else {
-    cudaFuncSetAttribute(k_paged_attn_2cta<64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Attn2Cfg<64>::kSmem);
-    cfg.dynamicSmemBytes = Attn2Cfg<64>::kSmem;
-    e = cudaOccupancyMaxActiveClusters(&n, k_paged_attn_2cta<64, true>, &cfg);
+    cudaFuncSetAttribute(k_paged_attn_2cta<64, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Attn2Cfg<64, true>::kSmem);
+    cfg.dynamicSmemBytes = Attn2Cfg<64, true>::kSmem;
+    e = cudaOccupancyMaxActiveClusters(&n, k_paged_attn_2cta<64, true, true>, &cfg);
   }
   if (e != cudaSuccess || n < 1) {
     cudaGetLastError();
