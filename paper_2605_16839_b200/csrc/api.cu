@@ -14,7 +14,7 @@
 
 namespace cpa {
 cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
-                          cudaStream_t st, int* launches);
+                          unsigned* tables_done, cudaStream_t st, int* launches);
 cudaError_t launch_block_scores(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
                                 const Geo& g, float* scores, int* mstar_key, int num_sms,
                                 cudaStream_t st, int* launches);
@@ -23,7 +23,7 @@ cudaError_t launch_block_scores_exact(const CUtensorMap& tq, const CUtensorMap& 
                                       int* launches);
 cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& g,
                           const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
-                          int* dev_status, int32_t* indptr, int32_t* indices, cudaStream_t st,
+                          int* dev_status, unsigned* done, int32_t* indptr, int32_t* indices, cudaStream_t st,
                           int* launches);
 cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
@@ -187,6 +187,7 @@ struct WS {
   float* scores;
   int* mstar_key;
   uint32_t* gwords;
+  unsigned* done;  // k_mask_union's last-CTA counter
   size_t total;
 };
 size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -202,6 +203,8 @@ WS carve(const Geo& g, void* base) {
   off += up256((size_t)g.B * g.Gn * g.Rpad * 4);
   w.gwords = reinterpret_cast<uint32_t*>(p + off);
   off += up256((size_t)g.B * g.Gn * g.nwords * 4);
+  w.done = reinterpret_cast<unsigned*>(p + off);
+  off += 256;
   w.total = off;
   return w;
 }
@@ -305,7 +308,8 @@ int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cp
           cudaSuccess)
         return cuda_fail(e, "block_scores_exact");
     } else {
-      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(q), g, w.qbar, w.mstar_key, st, launches)) != cudaSuccess)
+      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(q), g, w.qbar, w.mstar_key, w.done, st, launches)) !=
+          cudaSuccess)
         return cuda_fail(e, "pool_q");
       if ((e = launch_block_scores(tq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) != cudaSuccess)
         return cuda_fail(e, "block_scores");
@@ -318,9 +322,13 @@ int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cp
   if (mask_in && out->dev_status) {
     if ((e = cudaMemsetAsync(out->dev_status, 0, sizeof(int), st)) != cudaSuccess) return cuda_fail(e, "memset");
   }
+  // the pooled path's k_pool_q zeroes the tables counter; the other paths do it here
+  if (mask_in || (p->flags & CPA_F_EXACT_SCORES)) {
+    if ((e = cudaMemsetAsync(w.done, 0, sizeof(unsigned), st)) != cudaSuccess) return cuda_fail(e, "memset");
+  }
   e = launch_tables(scores, w.mstar_key, g, mask_in ? out->mask_bits : nullptr,
                     (!mask_in && (p->flags & CPA_F_MASK_OUT)) ? out->mask_bits : nullptr, w.gwords,
-                    mask_in ? out->dev_status : nullptr, out->kv_indptr, out->kv_indices, st, launches);
+                    mask_in ? out->dev_status : nullptr, w.done, out->kv_indptr, out->kv_indices, st, launches);
   if (e != cudaSuccess) return cuda_fail(e, "tables");
   return CPA_OK;
 }

@@ -13,20 +13,36 @@
 namespace cpa {
 
 // ---------------------------------------------------------------- a1: pool Q
-// grid (nqb, B, Hq*d/512), block 256 threads = 4 token quarters x 64 slab threads; a slab thread
-// owns 8 consecutive elements (one uint4) of a 512-element slice of [Hq*d]; each quarter sums a
-// quarter of the q-block's tokens (8 loads in flight), the quarters are combined in shared memory.
-// qbar: [2][B*Gn*Rpad][d] bf16 (hi rows, then lo rows).
-__global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
-                                                __nv_bfloat16* __restrict__ qbar, int* __restrict__ mstar_key) {
-  __shared__ float part[3][64][9];
+// grid (nqb + 1, B, ceil(Hq*d/512)), block 1024 threads = 16 token parts x 64 slab threads; a slab
+// thread owns 8 consecutive elements (one uint4) of a 512-element slice of [Hq*d]; each part sums
+// 1/16 of the q-block's tokens with all its loads in flight at once (8 for bs = 128), the parts are
+// combined in shared memory. Blocks x = nqb zero the padding rows [R, Rpad) of qbar (padded MMA rows
+// must be finite). qbar: [2][B*Gn*Rpad][d] bf16 (hi rows, then lo rows).
+constexpr int kPoolParts = 16;
+__global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
+                                                 __nv_bfloat16* __restrict__ qbar, int* __restrict__ mstar_key,
+                                                 unsigned* __restrict__ tables_done) {
+  __shared__ float part[kPoolParts - 1][64][9];
   const int i = blockIdx.x, b = blockIdx.y;
-  const int st = threadIdx.x & 63, quarter = threadIdx.x >> 6;
+  if (i == 0 && b == 0 && blockIdx.z == 0 && threadIdx.x == 0) *tables_done = 0u;  // k_mask_union's counter
+  const long long nrows = (long long)g.B * g.Gn * g.Rpad;
+  if (i == g.nqb) {  // padding rows of the groups z, z + gridDim.z, ... of batch b
+    const int npad = g.Rpad - g.R, per_row = g.d / 8;  // uint4 per row
+    for (int grp = blockIdx.z; grp < g.Gn; grp += gridDim.z)
+      for (int x = threadIdx.x; x < npad * per_row; x += blockDim.x) {
+        const long long row = ((long long)b * g.Gn + grp) * g.Rpad + g.R + x / per_row;
+        const int e = (x % per_row) * 8;
+        *reinterpret_cast<uint4*>(qbar + row * g.d + e) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(qbar + (nrows + row) * g.d + e) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    return;
+  }
+  const int st = threadIdx.x & 63, pt = threadIdx.x >> 6;
   const int x0 = (blockIdx.z * 64 + st) * 8;  // element offset in [0, Hq*d)
   const bool active = x0 < g.Hq * g.d;         // last slab may be partial (Hq*d % 512 != 0)
   const int p0 = i * g.bs, p1 = min(p0 + g.bs, g.C);
-  const int nq = (p1 - p0 + 3) / 4;
-  const int a0 = p0 + quarter * nq, a1 = active ? min(a0 + nq, p1) : a0;
+  const int nq = (p1 - p0 + kPoolParts - 1) / kPoolParts;
+  const int a0 = min(p0 + pt * nq, p1), a1 = active ? min(a0 + nq, p1) : a0;
   const uint4* src = reinterpret_cast<const uint4*>(q + (long long)b * g.b_stride + x0);
   const long long stride = g.q_stride / 8;  // uint4 per token
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -47,14 +63,13 @@ __global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict_
     for (int u = 0; u < 8; ++u) add(w[u]);
   }
   for (; p < a1; ++p) add(__ldg(src + (long long)p * stride));
-  if (quarter > 0) {
+  if (pt > 0) {
 #pragma unroll
-    for (int c = 0; c < 8; ++c) part[quarter - 1][st][c] = acc[c];
+    for (int c = 0; c < 8; ++c) part[pt - 1][st][c] = acc[c];
   }
   __syncthreads();
-  if (quarter != 0 || !active) return;
-#pragma unroll
-  for (int k = 0; k < 3; ++k)
+  if (pt != 0 || !active) return;
+  for (int k = 0; k < kPoolParts - 1; ++k)
 #pragma unroll
     for (int c = 0; c < 8; ++c) acc[c] += part[k][st][c];
   const int h = x0 / g.d, e = x0 % g.d;
@@ -69,25 +84,9 @@ __global__ void __launch_bounds__(256) k_pool_q(const __nv_bfloat16* __restrict_
   }
   const int grp = h / g.E, hl = h % g.E;
   const long long row = ((long long)b * g.Gn + grp) * g.Rpad + hl * g.nqb + i;
-  const long long nrows = (long long)g.B * g.Gn * g.Rpad;
   *reinterpret_cast<uint4*>(qbar + row * g.d + e) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   *reinterpret_cast<uint4*>(qbar + (nrows + row) * g.d + e) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   if (e == 0) mstar_key[row] = float_key(-INFINITY);
-}
-
-// zero the padding rows r in [R, Rpad) of qbar (keeps the padded MMA rows finite)
-__global__ void k_pool_pad(Geo g, __nv_bfloat16* __restrict__ qbar) {
-  const long long nrows = (long long)g.B * g.Gn * g.Rpad;
-  const int npad = g.Rpad - g.R;
-  const long long total = (long long)g.B * g.Gn * npad * g.d;
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total;
-       x += (long long)gridDim.x * blockDim.x) {
-    const long long e = x % g.d, t = x / g.d;
-    const long long bg = t / npad, r = g.R + t % npad;
-    const long long row = bg * g.Rpad + r;
-    qbar[row * g.d + e] = __float2bfloat16_rn(0.f);
-    qbar[(nrows + row) * g.d + e] = __float2bfloat16_rn(0.f);
-  }
 }
 
 // ---------------------------------------------------------------- a2: block scores
@@ -469,15 +468,11 @@ int score_smem_bytes(int d, int bs) {
 }
 
 cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
-                          cudaStream_t st, int* launches) {
-  k_pool_q<<<dim3(g.nqb, g.B, (g.Hq * g.d + 511) / 512), 256, 0, st>>>(q, g, qbar, mstar_key);
+                          unsigned* tables_done, cudaStream_t st, int* launches) {
+  // x = nqb: padding blocks (they return at once when Rpad == R)
+  k_pool_q<<<dim3(g.nqb + (g.Rpad > g.R ? 1 : 0), g.B, (g.Hq * g.d + 511) / 512), 1024, 0, st>>>(q, g, qbar, mstar_key,
+                                                                                                tables_done);
   ++*launches;
-  if (g.Rpad > g.R) {
-    const long long total = (long long)g.B * g.Gn * (g.Rpad - g.R) * g.d;
-    const int blocks = (int)((total + 255) / 256 < 1024 ? (total + 255) / 256 : 1024);
-    k_pool_pad<<<blocks, 256, 0, st>>>(g, qbar);
-    ++*launches;
-  }
   return cudaGetLastError();
 }
 

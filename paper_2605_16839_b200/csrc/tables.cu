@@ -11,13 +11,69 @@
 
 namespace cpa {
 
+// Exclusive-scan CSR of the G words (row-major over r = b*Gn + g, then word) by one CTA of any
+// multiple-of-32 size: per tile of blockDim words a block-wide scan of the popcounts with a running
+// carry, then every word scatters its set bits (ascending j within a row). gwords is read with
+// .cg loads: other CTAs of the same grid wrote it.
+__device__ void csr_block(const uint32_t* gwords, const Geo& g, int32_t* indptr, int32_t* indices) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry_s;
+  const int nrows = g.B * g.Gn;
+  const int total = nrows * g.nwords;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int base = 0; base < total; base += blockDim.x) {
+    const int x = base + tid;
+    const uint32_t word = x < total ? __ldcg(gwords + x) : 0u;
+    const int cnt = __popc(word);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int v = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (lane < nw) warp_sums[lane] = v;  // inclusive prefix of warp totals
+    }
+    __syncthreads();
+    const int carry = carry_s;
+    const int excl = carry + (wid > 0 ? warp_sums[wid - 1] : 0) + incl - cnt;
+    if (x < total) {
+      const int row = x / g.nwords, wi = x % g.nwords;
+      if (wi == 0) indptr[row] = excl;
+      uint32_t rem = word;
+      int pos = excl;
+      while (rem) {
+        const int bit = __ffs(rem) - 1;
+        rem &= rem - 1;
+        indices[pos++] = wi * 32 + bit;
+      }
+    }
+    __syncthreads();
+    if (tid == blockDim.x - 1) carry_s = carry + warp_sums[nw - 1];
+    __syncthreads();
+  }
+  if (tid == 0) indptr[nrows] = carry_s;
+}
+
 // One CTA per (word w of 32 kv blocks, execution group bg). Thread t handles estimator rows
 // r = t, t+blockDim, ... (r = hl*nqb + i). Each row forms its 32-bit mask word, the CTA ORs the
-// words of all its rows (Q-block union and intra-group union in one reduction).
+// words of all its rows (Q-block union and intra-group union in one reduction). The last CTA to
+// finish (device-scope counter `done`, zero on entry and reset on exit) builds the CSR tables.
 __global__ void __launch_bounds__(128)
     k_mask_union(const float* __restrict__ scores, const int* __restrict__ mstar_key, Geo g,
                  const uint32_t* __restrict__ mask_in, uint32_t* __restrict__ mask_out,
-                 uint32_t* __restrict__ gwords, int* __restrict__ dev_status) {
+                 uint32_t* __restrict__ gwords, int* __restrict__ dev_status, unsigned* __restrict__ done,
+                 int32_t* __restrict__ indptr, int32_t* __restrict__ indices) {
   const int w = blockIdx.x, bg = blockIdx.y;
   const int b = bg / g.Gn, grp = bg % g.Gn;
   const bool sink = (g.flags & 1u) != 0;
@@ -56,6 +112,7 @@ __global__ void __launch_bounds__(128)
   }
   acc = __reduce_or_sync(0xffffffffu, acc);
   __shared__ uint32_t red[32];
+  __shared__ bool last;
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -69,72 +126,23 @@ __global__ void __launch_bounds__(128)
         if (jbase + jj >= g.pb) need |= 1u << jj;
       if ((word & need) != need) atomicCAS(dev_status, 0, 1 + bg);
     }
+    __threadfence();  // publish the word before counting this CTA as done
+    last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
   }
-}
-
-// Single CTA: popcounts of all G words (row-major over r = b*Gn + g, then word), one block-wide
-// exclusive scan per 1024-word tile with a running carry, then every word scatters its set bits.
-__global__ void __launch_bounds__(1024)
-    k_csr(const uint32_t* __restrict__ gwords, Geo g, int32_t* __restrict__ indptr,
-          int32_t* __restrict__ indices) {
-  __shared__ int warp_sums[32];
-  __shared__ int carry_s;
-  const int nrows = g.B * g.Gn;
-  const int total = nrows * g.nwords;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) carry_s = 0;
   __syncthreads();
-  for (int base = 0; base < total; base += blockDim.x) {
-    const int x = base + tid;
-    const uint32_t word = x < total ? gwords[x] : 0u;
-    const int cnt = __popc(word);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (lane == 31) warp_sums[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-      const int nw = blockDim.x >> 5;
-      int v = lane < nw ? warp_sums[lane] : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += y;
-      }
-      if (lane < nw) warp_sums[lane] = v;  // inclusive prefix of warp totals
-    }
-    __syncthreads();
-    const int carry = carry_s;
-    const int excl = carry + (wid > 0 ? warp_sums[wid - 1] : 0) + incl - cnt;
-    if (x < total) {
-      const int row = x / g.nwords, wi = x % g.nwords;
-      if (wi == 0) indptr[row] = excl;
-      uint32_t rem = word;
-      int pos = excl;
-      while (rem) {
-        const int bit = __ffs(rem) - 1;
-        rem &= rem - 1;
-        indices[pos++] = wi * 32 + bit;
-      }
-    }
-    __syncthreads();
-    if (tid == blockDim.x - 1) carry_s = carry + warp_sums[(blockDim.x >> 5) - 1];
-    __syncthreads();
-  }
-  if (tid == 0) indptr[nrows] = carry_s;
+  if (!last) return;
+  __threadfence();
+  csr_block(gwords, g, indptr, indices);
+  if (threadIdx.x == 0) *done = 0u;  // ready for the next call
 }
 
 cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& g,
                           const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
-                          int* dev_status, int32_t* indptr, int32_t* indices, cudaStream_t st,
+                          int* dev_status, unsigned* done, int32_t* indptr, int32_t* indices, cudaStream_t st,
                           int* launches) {
   k_mask_union<<<dim3(g.nwords, g.B * g.Gn), 128, 0, st>>>(scores, mstar_key, g, mask_in, mask_out,
-                                                           gwords, dev_status);
-  k_csr<<<1, 1024, 0, st>>>(gwords, g, indptr, indices);
-  *launches += 2;
+                                                           gwords, dev_status, done, indptr, indices);
+  *launches += 1;
   return cudaGetLastError();
 }
 
