@@ -283,7 +283,8 @@ def run_gpu(args):
             step()
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        # thread_local: the NCCL watchdog thread may query events while this thread captures
+        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
             step()
         torch.cuda.synchronize()
         direct_step = step
