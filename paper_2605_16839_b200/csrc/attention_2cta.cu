@@ -270,7 +270,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* pv_done = p_full + 4;                   // both [2]: last P.V into O_w complete
   uint64_t* o_full = pv_done + 2;                   // both: every MMA of the item complete
   uint64_t* o_empty = o_full + 1;                   // leader: epilogue read O (16 warp arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  uint64_t* stag = o_empty + 1;                     // local [4][2]: WG0 quarter q done with page's max
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stag + 8);
   int* total_s = reinterpret_cast<int*>(tmem_slot + 1);
   int* single_s = total_s + 1;  // non-persistent unit: {unit, start, n, nd}
 
@@ -298,6 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     mbar_init(pv_done + 1, 1);
     mbar_init(o_full, 1);
     mbar_init(o_empty, 16);  // 8 softmax warps x 2 CTAs
+    for (int i = 0; i < 8; ++i) mbar_init(stag + i, 1);
     fence_barrier_init();
     if constexpr (!PERSIST) {  // one cluster = one whole unit
       int s, n, nd;
@@ -513,11 +515,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       for (int t = ta; t < te; ++t, ++n) {
         const uint32_t s_tm = s_tm0 + (n & 1) * 128;
         if (row == 0) TRACE2(4 + 16 * wg, n);
+#ifndef CPA_NO_STAGGER
+        // WG1 starts a page when WG0 (same rows, same SMSP) has finished its TMEM load + block max of
+        // that page, so one warp's non-MUFU phase overlaps the other's exponentials
+        if (wg == 1) mbar_wait(stag + quarter * 2 + (n & 1), (n >> 1) & 1);
+#endif
         mbar_wait(s_full + (n & 1), (n >> 1) & 1);
         if (row == 0) TRACE2(5 + 16 * wg, n);
         tc_fence_after();
 #ifdef CPA_EXP_NO_SOFTMAX  // A/B only: MMA / TMA / converter pipeline alone (wrong results)
         __syncwarp();
+#ifndef CPA_NO_STAGGER
+        if (wg == 0 && lane == 0) mbar_arrive(stag + quarter * 2 + (n & 1));
+#endif
         if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
         continue;
 #endif
@@ -551,6 +561,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
         const float m_use = (m_run == -INFINITY) ? 0.f : m_run;
         if (row == 0) TRACE2(11 + 16 * wg, n);
+#ifndef CPA_NO_STAGGER
+        if (wg == 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(stag + quarter * 2 + (n & 1));
+        }
+#endif
         // P = exp2(s*sl2 - m): packed f32x2 FFMA; pairs chosen by use_poly_exp on a degree-3
         // polynomial (FMA pipe), the rest on MUFU.EX2; 4 partial f32x2 sums; fp16 pack; stored over S.
         float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
