@@ -237,14 +237,17 @@ def run_gpu(args):
     nkvb = -(-L // bs)
     pt, npages = page_layout(cfg.batch, nkvb, seed)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
-    cache = cpa.PagedKVCache(dev(to_pool(k, pt, npages, bs)), dev(to_pool(v, pt, npages, bs)),
-                             torch.from_numpy(pt).cuda())
+    vpool = dev(to_pool(v, pt, npages, bs))
+    if args.v_f16:  # CPA_F_V_F16: the V pool holds fp16 (exact for these bf16 values)
+        vpool = vpool.half()
+    cache = cpa.PagedKVCache(dev(to_pool(k, pt, npages, bs)), vpool, torch.from_numpy(pt).cuda())
     dq = dev(q)
     kc = dev(k[:, :, P:].transpose(0, 2, 1, 3))  # the chunk's own K/V [B, C, Hkv, d] (re-appended)
     vc = dev(v[:, :, P:].transpose(0, 2, 1, 3))
     E_exec = args.exec_group or E
+    vflag = cpa.F_V_F16 if args.v_f16 else 0
     p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
-                        flags=cpa.F_EXACT_SCORES if args.exact_scores else 0)
+                        flags=(cpa.F_EXACT_SCORES if args.exact_scores else 0) | vflag)
     tables = cpa.alloc_tables(p)
     ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
     o = torch.empty(cfg.batch, C, hq_l, d, dtype=torch.bfloat16, device="cuda")
@@ -359,7 +362,7 @@ def run_gpu(args):
     density = (ip[-1] - cfg.batch * Gx * (nkvb - P // bs)) / (cfg.batch * Gx * (P // bs))
     # per-stage sparsity from the GPU's own mask bits (one extra build, outside the timed region)
     pm = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
-                         flags=cpa.F_MASK_OUT | (cpa.F_EXACT_SCORES if args.exact_scores else 0))
+                         flags=cpa.F_MASK_OUT | (cpa.F_EXACT_SCORES if args.exact_scores else 0) | vflag)
     tm = cpa.alloc_tables(pm, mask=True)
     cpa.build_tables(pm, dq, cache, tm)
     nqb = -(-C // bs)
@@ -430,7 +433,8 @@ def run_gpu(args):
                        "block_size": bs, "alpha": ALPHA, "needle_density": RHO, "exec_group_size": E_exec,
                        "scorer": "exact tile max (SPEC.md:223)" if args.exact_scores else "pooled query (SPEC.md:269)",
                        "parallelism": f"kv-group shard x{world}" + (f" + {collective}" if collective != "none" else ""),
-                       "l2": "flushed (512 MiB write) before every timed step", "launch": launch},
+                       "l2": "flushed (512 MiB write) before every timed step", "launch": launch,
+                       "v_cache_dtype": "f16" if args.v_f16 else "bf16"},
             "dense_ms_per_chunk": round(t_dense, 4),
             "speedup_vs_dense": round(t_dense / ms, 3),
             "attention_only_speedup": round(t_dense / t_attn, 3),
@@ -497,6 +501,9 @@ def main():
                     help="execution-group size E (0 = full KV group; 4 = sub-KV-group union, PAPER.md:498)")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph")
+    ap.add_argument("--v-bf16", dest="v_f16", action="store_false",
+                    help="keep the V pool in bf16 (converted per page inside the attention kernel) instead of the "
+                         "default fp16 pool (CPA_F_V_F16: converted once at append; bitwise-identical outputs)")
     ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
                     help="N>1 head-output all-gather: fused P2P stores in the attention epilogue, or NCCL")
     args = ap.parse_args()

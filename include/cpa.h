@@ -79,7 +79,11 @@ enum {
   CPA_F_P_BF16 = 256u,    /* ablation: round softmax P to bf16 instead of fp16 before P.V (K3) */
   CPA_F_NO_2CTA = 512u,   /* ablation: single-CTA attention kernel instead of the cta_group::2 pair */
   CPA_F_NO_PERSIST = 1024u, /* ablation: one cluster per work unit instead of the persistent stream-K grid */
-  CPA_F_PERSIST = 2048u   /* ablation / tests: persistent stream-K grid whenever B*Gn <= 4 */
+  CPA_F_PERSIST = 2048u,  /* ablation / tests: persistent stream-K grid whenever B*Gn <= 4 */
+  CPA_F_V_F16 = 4096u     /* the V pool holds fp16 (cpa_append_kv converts the bf16 chunk; exact for bf16
+                             values in fp16's normal range, i.e. the conversion the attention kernels
+                             otherwise do per page): the attention kernels skip their V conversion.
+                             Incompatible with CPA_F_P_BF16. */
 };
 
 typedef struct {

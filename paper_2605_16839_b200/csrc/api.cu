@@ -139,6 +139,8 @@ int make_geo(const cpa_params* p, Geo* g) {
     return fail(CPA_ERR_UNSUPPORTED, "block_size must be 16, 32, 64 or 128");
   if (p->prefix_len % bs) return fail(CPA_ERR_MISALIGNED, "prefix_len %% block_size != 0");
   if (!(p->alpha > 0.f && p->alpha <= 1.f)) return fail(CPA_ERR_ALPHA, "alpha must be in (0, 1]");
+  if ((p->flags & CPA_F_V_F16) && (p->flags & CPA_F_P_BF16))
+    return fail(CPA_ERR_UNSUPPORTED, "CPA_F_V_F16 needs fp16 P (not CPA_F_P_BF16)");
   const long long qs = p->q_token_stride ? p->q_token_stride : (long long)p->num_q_heads * p->head_dim;
   if (qs < (long long)p->num_q_heads * p->head_dim || qs % 8)
     return fail(CPA_ERR_MISALIGNED, "q_token_stride must be >= Hq*d and a multiple of 8");

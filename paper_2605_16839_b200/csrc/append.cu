@@ -23,7 +23,14 @@ __global__ void __launch_bounds__(256) k_append(const uint4* __restrict__ kc, co
     const int page = __ldg(pt + (long long)b * g.maxb + j);
     const long long dst = ((long long)page * ps + (long long)h * hs + (long long)slot * g.d) / 8 + e;
     kp[dst] = kc[x];
-    vp[dst] = vc[x];
+    uint4 w = vc[x];
+    if (g.flags & CPA_F_V_F16) {  // V pool in fp16 (exact for bf16 values in fp16's normal range)
+      w.x = bf16x2_to_f16x2(w.x);
+      w.y = bf16x2_to_f16x2(w.y);
+      w.z = bf16x2_to_f16x2(w.z);
+      w.w = bf16x2_to_f16x2(w.w);
+    }
+    vp[dst] = w;
   }
 }
 

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(AttnCfg<D, BS, NT>::kThreads, 1)
     for (int n = 0; n < N; ++n) {
       const int vs = n % Cfg::kVStages;
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
-      if constexpr (PF16) {
+      if (PF16 && !(g.flags & (1u << 12))) {  // CPA_F_V_F16: the pool already holds fp16 V
         uint4* tile = reinterpret_cast<uint4*>(sV + vs * Cfg::kKVBytes);
 #pragma unroll 4
         for (int x = ct; x < Cfg::kKVBytes / 16; x += Cfg::kConvWarps * 32) {

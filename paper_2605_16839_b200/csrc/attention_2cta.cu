@@ -466,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
       if (ct == 0) TRACE2(7, n);
 #ifndef CPA_EXP_NO_CONV
-      if constexpr (PF16) {
+      if (PF16 && !(g.flags & (1u << 12))) {  // CPA_F_V_F16: the pool already holds fp16 V
 #else
       if constexpr (false) {
 #endif

@@ -433,3 +433,32 @@ def test_persistent_stream_k_small_shapes(B, Hq, Hkv, bs, C, P):
     t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
     got = _gpu_attn(case, t)
     assert rel_err(got, O.paged_attention(q, k, v, P, bs, ip, ix)) <= ATOL_REL
+
+
+@pytest.mark.parametrize("cfg_name", ["tiny", "llama8b_32k"])
+def test_v_f16_pool_bitwise(cfg_name):
+    """CPA_F_V_F16: a V pool holding fp16 (prefix converted on the host, the chunk by cpa_append_kv)
+    gives exactly the outputs of the bf16 pool (the kernels' per-page conversion is the same rounding)."""
+    cfg = CONFIGS[cfg_name]
+    seed = 16839
+    k, v = make_kv(cfg, seed)
+    q = make_q(cfg, seed)
+    P, C, L = cfg.chunk_geometry()
+    bs = cfg.block_size
+    case = Case(q, k, v, P, bs, seed=seed)
+    kc = to_dev_bf16(k[:, :, P:].transpose(0, 2, 1, 3))
+    vc = to_dev_bf16(v[:, :, P:].transpose(0, 2, 1, 3))
+    outs = []
+    for flag in (0, cpa.F_V_F16):
+        vp = case.cache.v_pages.clone()
+        if flag:
+            vp = vp.half()  # exact: bf16 values in fp16's range
+        cache = cpa.PagedKVCache(case.cache.k_pages, vp, case.cache.page_table)
+        p = cpa.make_params(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, flags=flag)
+        o = case.out(f32=False)
+        cpa.chunk_step(p, case.dq, cache, cpa.alloc_tables(p), o, kc, vc)
+        torch.cuda.synchronize()
+        outs.append(o.clone())
+        if flag:  # the append's device conversion of the chunk's V == the host's round-to-nearest
+            assert torch.equal(vp, case.cache.v_pages.half())
+    assert torch.equal(outs[0], outs[1])
