@@ -280,6 +280,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const int cl = (int)blockIdx.x >> 1;
   const uint32_t warp = warp_id(), lane = lane_id();
   constexpr uint32_t kConvWarp0 = 8, kTmaWarp = 10, kMmaWarp = 11;
+  const bool vf16 = PF16 && (g.flags & (1u << 12)) != 0;  // CPA_F_V_F16: V pages already fp16
 
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch_desc(&tm_q);
@@ -357,8 +358,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           __syncwarp();
           mbar_wait(v_empty + vs, ((n / Cfg::kVStages) & 1) ^ 1);
           if (elect_one()) {
-            mbar_expect_tx(v_full + vs, Cfg::kVHalf);
-            tma_load_4d(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+            if (vf16) {  // fp16 pool: both halves signal the leader's v_full directly (no conversion relay)
+              if (leader) mbar_expect_tx(v_full + vs, 2 * Cfg::kVHalf);
+              tma_load_4d_2sm(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+            } else {
+              mbar_expect_tx(v_full + vs, Cfg::kVHalf);
+              tma_load_4d(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+            }
           }
           __syncwarp();
         }
@@ -439,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const int i = it.idx;
         for (int t = it.a; t < it.e; ++t, ++n) {
           const bool first = t == it.a, last = t + 1 == it.e;
-          mbar_wait(v_ready + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
+          mbar_wait((vf16 ? v_full : v_ready) + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
           if (lane == 0) TRACE2(1, n);
           if (PERSIST && first && i > 0) mbar_wait(o_empty, (i - 1) & 1);  // previous item's O read out of TMEM
           mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
@@ -461,7 +467,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
   } else if (warp >= kConvWarp0) {  // --------------------------------------- V bf16 -> fp16
     const int ct = (warp - kConvWarp0) * 32 + lane;
-    for (int n = 0; n < G; ++n) {
+    for (int n = 0; n < (vf16 ? 0 : G); ++n) {  // fp16 pool: nothing to convert or relay
       const int vs = n % Cfg::kVStages;
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
       if (ct == 0) TRACE2(7, n);

@@ -14,7 +14,9 @@ E_ = cfg.num_q_heads // cfg.num_kv_heads
 k, v = make_kv(cfg, seed, kv_heads=range(KVH)); q = make_q(cfg, seed, q_heads=range(KVH * E_))
 pt, npg = page_layout(cfg.batch, -(-L // bs), seed)
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
-cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)), torch.from_numpy(pt).cuda())
+VF16 = os.environ.get("V_F16", "1") == "1"  # default: the fp16 V pool of the product path (CPA_F_V_F16)
+vpool = dev(to_pool(v, pt, npg, bs))
+cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), vpool.half() if VF16 else vpool, torch.from_numpy(pt).cuda())
 dq = dev(q); del k, v
 p = cpa.make_params(cfg.batch, KVH * E_, KVH, cfg.head_dim, bs, C, P, alpha=0.06)
 flag_sets = [int(x, 0) for x in os.environ.get("FLAGSETS", "0").split(",")]
@@ -35,7 +37,7 @@ for r in range(rounds):
     for (path, fl) in order:
         cpa._lib = libs.get(path); cpa.LIB_PATH = path
         cpa.lib(); libs[path] = cpa._lib
-        p.flags = (p.flags & 1) | fl
+        p.flags = (p.flags & 1) | fl | (cpa.F_V_F16 if VF16 else 0)
         if tabs is None:
             tabs = cpa.alloc_tables(p); cpa.build_tables(p, dq, cache, tabs)
         for name, tab in (("sparse", tabs), ("dense", None)):
