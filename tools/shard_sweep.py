@@ -39,11 +39,13 @@ def main():
         k, v = make_kv(cfg, seed, 0.30, kv_heads=kvh)
         q = dev(make_q(cfg, seed, q_heads=qh))
         pt, npg = page_layout(cfg.batch, nkvb, seed)
-        cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)), torch.from_numpy(pt).cuda())
+        # fp16 V pool, as bench.py (CPA_F_V_F16)
+        cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)).half(),
+                                 torch.from_numpy(pt).cuda())
         kc, vc = dev(k[:, :, P:].transpose(0, 2, 1, 3)), dev(v[:, :, P:].transpose(0, 2, 1, 3))
         res = {}
         for name, extra in (("auto", 0), ("per_unit_grid", cpa.F_NO_PERSIST)):
-            p = cpa.make_params(cfg.batch, len(qh), len(kvh), d, bs, C, P, alpha=0.06, flags=extra)
+            p = cpa.make_params(cfg.batch, len(qh), len(kvh), d, bs, C, P, alpha=0.06, flags=extra | cpa.F_V_F16)
             t = cpa.alloc_tables(p)
             ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
             o = torch.empty(cfg.batch, C, len(qh), d, dtype=torch.bfloat16, device="cuda")
