@@ -462,3 +462,36 @@ def test_v_f16_pool_bitwise(cfg_name):
         if flag:  # the append's device conversion of the chunk's V == the host's round-to-nearest
             assert torch.equal(vp, case.cache.v_pages.half())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_v_f16_pool_other_paths_bitwise():
+    """CPA_F_V_F16 on the 1-CTA kernel (d=64), the copy ablation and block-sparse execution: the fp16
+    pool gives exactly the bf16-pool outputs on every attention entry point."""
+    Hq, Hkv, C, P = 8, 2, 256, 6 * 128
+    for d, bs in ((64, 32), (128, 128)):
+        q, k, v = random_qkv(1, Hq, Hkv, d, C, P + C, seed=d + bs)
+        case = Case(q, k, v, P, bs, seed=4)
+        nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+        M = random_block_mask(1, Hq, nqb, nkvb, 0.3, seed=bs)
+        for i in range(nqb):
+            M[:, :, i, pb + i + 1:] = False
+            M[:, :, i, pb:pb + i + 1] = True
+        ip, ix = O.tables_from_mask(M, case.E, pb)
+        t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
+        bits = torch.from_numpy(mask_to_bits(M)).cuda()
+        res = {}
+        for flag in (0, cpa.F_V_F16):
+            vp = case.cache.v_pages.half() if flag else case.cache.v_pages
+            cache = cpa.PagedKVCache(case.cache.k_pages, vp, case.cache.page_table)
+            p = cpa.make_params(1, Hq, Hkv, d, bs, C, P, flags=cpa.F_OUT_F32 | cpa.F_NO_PERSIST | flag)
+            outs = []
+            for fn in (lambda o: cpa.paged_attention(p, case.dq, cache, t, o),
+                       lambda o: cpa.paged_attention_copy(p, case.dq, cache, t, o)) + \
+                    ((lambda o: cpa.block_sparse_attention(p, case.dq, cache, bits, o)),) * (bs == 128):
+                o = case.out(True)
+                fn(o)
+                outs.append(o)
+            torch.cuda.synchronize()
+            res[flag] = outs
+        for a, b in zip(res[0], res[cpa.F_V_F16]):
+            assert torch.equal(a, b)
