@@ -34,12 +34,12 @@ def run(context, chunk, alpha=0.06, seed=16839, reps=3):
     pt, npg = page_layout(B, nkvb, seed)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
     kp = torch.zeros(npg, Hkv, bs, d, dtype=torch.bfloat16, device="cuda")
-    vp = torch.zeros_like(kp)
+    vp = torch.zeros(npg, Hkv, bs, d, dtype=torch.float16, device="cuda")  # fp16 V pool (CPA_F_V_F16)
     cache = cpa.PagedKVCache(kp, vp, torch.from_numpy(pt).cuda())
     chunks = []
     for t in range(cfg.num_chunks):
         P, C, L = cfg.chunk_geometry(t)
-        p = cpa.make_params(B, Hq, Hkv, d, bs, C, P, alpha=alpha)
+        p = cpa.make_params(B, Hq, Hkv, d, bs, C, P, alpha=alpha, flags=cpa.F_V_F16)
         chunks.append(dict(p=p, q=dev(make_q(cfg, seed, chunk_index=t)),
                            kc=dev(k[:, :, P:L].transpose(0, 2, 1, 3)), vc=dev(v[:, :, P:L].transpose(0, 2, 1, 3)),
                            o=torch.empty(B, C, Hq, d, dtype=torch.bfloat16, device="cuda")))
