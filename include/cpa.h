@@ -113,7 +113,7 @@ typedef struct {
  * zero-initialised by the caller; SURVEY §7 hard part 7). */
 typedef struct {
   void* k_pages;                /* bf16 (written only by cpa_append_kv / cpa_chunk_step append) */
-  void* v_pages;                /* bf16 */
+  void* v_pages;                /* bf16, or fp16 with CPA_F_V_F16 (same layout) */
   int64_t page_stride;          /* elements; 0 => Hkv*bs*d */
   int64_t head_stride;          /* elements; 0 => bs*d */
   const int32_t* page_table;    /* int32 [B, max_blocks_per_seq], device */
