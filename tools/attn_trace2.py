@@ -11,9 +11,12 @@ P, C, L = cfg.chunk_geometry(); bs = cfg.block_size
 k, v = make_kv(cfg, seed); q = make_q(cfg, seed)
 pt, npg = page_layout(cfg.batch, -(-L // bs), seed)
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
-cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)), torch.from_numpy(pt).cuda())
+VF16 = os.environ.get("V_F16", "1") == "1"  # fp16 V pool (product default)
+vpool = dev(to_pool(v, pt, npg, bs))
+cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), vpool.half() if VF16 else vpool, torch.from_numpy(pt).cuda())
 dq = dev(q)
-p = cpa.make_params(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06)
+p = cpa.make_params(cfg.batch, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06,
+                    flags=cpa.F_V_F16 if VF16 else 0)
 o = torch.empty(cfg.batch, C, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
 t = cpa.alloc_tables(p); cpa.build_tables(p, dq, cache, t)
 for _ in range(3): cpa.paged_attention(p, dq, cache, t, o)
