@@ -393,7 +393,8 @@ def run_gpu(args):
         # the same public API fed from pinned host buffers as a serving loop would: HostChunkStream
         # overlaps step i+1's H2D and step i-1's D2H with step i's kernels; the timed region spans all
         # K steps (first H2D to last D2H, CUDA events), every copy inside it.
-        runner = cpa.HostChunkStream(p, cache, tables, tuple(dq.shape), tuple(kc.shape), workspace=ws)
+        runner = cpa.HostChunkStream(p, cache, tables, tuple(dq.shape), tuple(kc.shape), workspace=ws,
+                                     graphs=not args.no_graph)
         outs = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for _ in range(2)]
         for i in range(max(2, args.warmup)):
             runner.submit(hq_pin, outs[i & 1], hk_pin, hv_pin)

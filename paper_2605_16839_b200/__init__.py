@@ -307,10 +307,11 @@ class HostChunkStream:
     """Chunk steps fed from pinned HOST buffers, pipelined over three streams: the H2D copy of step
     i+1's inputs and the D2H copy of step i-1's output overlap step i's kernels (device staging is
     double-buffered; the cache, tables and workspace are used in stream order on the compute stream).
-    Plumbing only -- every step runs cpa_chunk_step. Read a host output only after synchronize()."""
+    Plumbing only -- every step runs cpa_chunk_step (with graphs=True replayed from one captured CUDA
+    graph per staging slot). Read a host output only after synchronize()."""
 
     def __init__(self, p: Params, cache: PagedKVCache, tables: BlockTables, q_shape, kv_shape,
-                 workspace: Optional[torch.Tensor] = None, device="cuda"):
+                 workspace: Optional[torch.Tensor] = None, device="cuda", graphs: bool = False):
         self.p, self.cache, self.tables = p, cache, tables
         self.ws = workspace if workspace is not None else _ws(p, None, device)
         bf = torch.bfloat16
@@ -324,6 +325,21 @@ class HostChunkStream:
         self.ev_comp = [torch.cuda.Event() for _ in range(2)]
         self.ev_out = [torch.cuda.Event() for _ in range(2)]
         self.i = 0
+        self.graphs = None
+        if graphs:  # one graph per slot: append + estimator + tables + attention on that slot's buffers
+            self.graphs = []
+            for s in range(2):
+                step = lambda s=s: chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s], self.k[s],
+                                              self.v[s], workspace=self.ws)
+                with torch.cuda.stream(self.s_comp):
+                    for _ in range(2):
+                        step()
+                self.s_comp.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.s_comp):
+                    step()
+                self.graphs.append(g)
+            torch.cuda.synchronize()
 
     def submit(self, hq: torch.Tensor, ho: torch.Tensor, hk: Optional[torch.Tensor] = None,
                hv: Optional[torch.Tensor] = None) -> None:
@@ -338,9 +354,14 @@ class HostChunkStream:
             self.ev_in[s].record(self.s_in)
         self.s_comp.wait_event(self.ev_in[s])
         self.s_comp.wait_event(self.ev_out[s])       # D2H of step i-2 has finished reading o[s]
-        chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s],
-                   self.k[s] if hk is not None else None, self.v[s] if hk is not None else None,
-                   workspace=self.ws, stream=self.s_comp)
+        if self.graphs is not None:  # the captured step always appends the slot's K/V
+            assert hk is not None, "graphs=True runs the step with the chunk's K/V"
+            with torch.cuda.stream(self.s_comp):
+                self.graphs[s].replay()
+        else:
+            chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s],
+                       self.k[s] if hk is not None else None, self.v[s] if hk is not None else None,
+                       workspace=self.ws, stream=self.s_comp)
         self.ev_comp[s].record(self.s_comp)
         self.s_out.wait_event(self.ev_comp[s])
         with torch.cuda.stream(self.s_out):

@@ -12,8 +12,8 @@ from tests.gpu_helpers import to_dev_bf16
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("cfg_name", ["tiny", "llama8b_32k"])
-def test_host_stream_matches_chunk_step(cfg_name):
+@pytest.mark.parametrize("cfg_name,graphs", [("tiny", False), ("llama8b_32k", False), ("llama8b_32k", True)])
+def test_host_stream_matches_chunk_step(cfg_name, graphs):
     cfg = CONFIGS[cfg_name]
     seed = 16839
     k, v = make_kv(cfg, seed)
@@ -34,7 +34,7 @@ def test_host_stream_matches_chunk_step(cfg_name):
         cpa.chunk_step(p, q, cache, t_ref, o, kc, vc)
         refs.append(o.cpu())
     torch.cuda.synchronize()
-    runner = cpa.HostChunkStream(p, cache, cpa.alloc_tables(p), tuple(qs[0].shape), tuple(kc.shape))
+    runner = cpa.HostChunkStream(p, cache, cpa.alloc_tables(p), tuple(qs[0].shape), tuple(kc.shape), graphs=graphs)
     hq = [q.cpu().pin_memory() for q in qs]
     hk, hv = kc.cpu().pin_memory(), vc.cpu().pin_memory()
     ho = [torch.full(q.shape, float("nan"), dtype=torch.bfloat16).pin_memory() for q in qs]
