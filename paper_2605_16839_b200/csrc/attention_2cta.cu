@@ -560,7 +560,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
               m4[w4] = fmax3(m4[w4], __uint_as_float(sv[k][c + 2 * w4]), __uint_as_float(sv[k][c + 2 * w4 + 1]));
         const float m_blk = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl2;
         float f = 1.f;
-        const bool rescale = m_blk > m_run + 8.0f;  // lazy rescale (first block always lands here)
+#ifndef CPA_RESCALE_THRESH
+#define CPA_RESCALE_THRESH 8.0f
+#endif
+        const bool rescale = m_blk > m_run + CPA_RESCALE_THRESH;  // lazy rescale (first block always lands here)
         if (rescale) {
           if (m_run != -INFINITY) f = fast_exp2(m_run - m_blk);
           m_run = m_blk;
