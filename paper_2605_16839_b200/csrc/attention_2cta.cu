@@ -413,7 +413,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       };
       // O_w += P_w V_n[w-half keys]: WG w's P (keys [w BS/2, (w+1) BS/2) of page n, fp16 packed over its
       // S^b columns) times those V rows; M=256, N=d (64 cols per CTA), K=BS/2
-      auto issue_pv = [&](int n, int w, bool first, bool last) {
+      // commits == false: the caller commits later (P.V(n,1) -> S(n+2) back to back, commits after)
+      auto issue_pv = [&](int n, int w, bool first, bool last, bool commits = true) {
         const uint32_t p_tm = tmem + (n & 1) * 128 + w * (BS / 2);
         const uint32_t o_tm = tmem + 256 + w * 128;
         const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kVHalf + w * (BS / 2) * 128;
@@ -423,11 +424,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
             mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
           }
-          tc_commit2(pv_done + w);
-          if (w == 1) {
-            tc_commit2(v_empty + n % Cfg::kVStages);
-            if (last) tc_commit2(o_full);
+          if (commits) {
+            tc_commit2(pv_done + w);
+            if (w == 1) {
+              tc_commit2(v_empty + n % Cfg::kVStages);
+              if (last) tc_commit2(o_full);
+            }
           }
+        }
+        __syncwarp();
+      };
+      auto pv1_commits = [&](int n, bool last) {
+        if (elect_one()) {
+          tc_commit2(pv_done + 1);
+          tc_commit2(v_empty + n % Cfg::kVStages);
+          if (last) tc_commit2(o_full);
         }
         __syncwarp();
       };
@@ -452,6 +463,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (lane == 0) TRACE2(2, n);
           tc_fence_after();
           issue_pv(n, 0, first, last);
+#ifndef CPA_NO_MMA_REORDER
+          if constexpr (!PERSIST) {
+          // the loop's critical latency is P(n, WG1) -> P.V(n,1) -> S(n+2) -> WG0's page n+2: wait for
+          // K(n+2) before P(n,1), issue P.V(n,1) and S(n+2) back to back, commit P.V(n,1)'s barriers after
+          // (per-unit grid only: in the persistent grid this order broke parity)
+          const bool more = n + 2 < G;
+          if (more) wait_k(n + 2);
+          mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+          tc_fence_after();
+          issue_pv(n, 1, first, last, false);
+          if (lane == 0) TRACE2(9, n);
+          if (more) issue_s(n + 2);
+          pv1_commits(n, last);
+          } else {
           mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
           tc_fence_after();
           issue_pv(n, 1, first, last);
@@ -461,6 +486,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             if (lane == 0) TRACE2(10, n);
             issue_s(n + 2);
           }
+          }
+#else
+          mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+          tc_fence_after();
+          issue_pv(n, 1, first, last);
+          if (lane == 0) TRACE2(9, n);
+          if (n + 2 < G) {
+            wait_k(n + 2);
+            if (lane == 0) TRACE2(10, n);
+            issue_s(n + 2);
+          }
+#endif
           if (lane == 0) TRACE2(3, n);
         }
       }
