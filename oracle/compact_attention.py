@@ -26,6 +26,9 @@ Parity status:
   threshold_mask ................. pinned (SPEC.md:236-238 worked examples, boundaries)
   block_scores_pooled ............ pinned (brute-force tile max; pooled == exact when a
                                    q-block's queries are identical)
+  block_scores_exact ............. pinned (pure-Python brute force over the explicit causal
+                                   (p, t) pair set incl. partial diagonal tiles, SPEC.md:223, 228;
+                                   planted per-query causal-limit case)
   pooled estimator on real model activations: parity unpinned (the paper prints no
   scores, masks or FlashPrefill formula).
 """

@@ -232,6 +232,53 @@ def test_pooled_scores_brute_force():
                 assert abs(m[0, h, i, j] - best) < 1e-12
 
 
+@pytest.mark.parametrize("C,seed", [(7, 41), (12, 42), (16, 43)])
+def test_exact_scores_brute_force(C, seed):
+    # SPEC.md:223 (tile max over every causal (query, key) pair of the tile, t <= P + p for EACH
+    # query p) and SPEC.md:228 ("random instance -> per-tile max-logit agrees with brute-force max
+    # over the tile"). Distinct queries, partial last q-block / kv-block, diagonal tiles included:
+    # pure-Python dot products over the explicit pair set, no matmul, no block arithmetic reuse.
+    B, Hq, Hkv, d, bs, P = 1, 4, 2, 4, 4, 8
+    L = P + C
+    q, k, _ = random_qkv(B, Hq, Hkv, d, C, L, seed=seed)
+    m = O.block_scores_exact(q, k, P, bs)
+    scale = 1.0 / math.sqrt(d)
+    nqb, nkvb = -(-C // bs), -(-L // bs)
+    assert m.shape == (B, Hq, nqb, nkvb)
+    for h in range(Hq):
+        kvh = h // (Hq // Hkv)
+        for i in range(nqb):
+            for j in range(nkvb):
+                pairs = [(p, t) for p in range(C) if p // bs == i
+                         for t in range(L) if t // bs == j and t <= P + p]
+                if not pairs:
+                    assert m[0, h, i, j] == -np.inf, (h, i, j)
+                    continue
+                best = max(scale * sum(float(q[0, p, h, e]) * float(k[0, kvh, t, e]) for e in range(d))
+                           for p, t in pairs)
+                assert abs(m[0, h, i, j] - best) < 1e-12, (h, i, j)
+
+
+def test_exact_scores_per_query_causal_limit():
+    # on a diagonal tile a key is visible only to the queries at or after it. Plant a
+    # key at chunk position 3 that aligns with query 0 only (query 0 cannot see it: 3 > 0), and make
+    # query 3 orthogonal to it: the exact tile max must NOT contain that pair, while the pooled
+    # scorer (union limit t <= P + last_p, R6) does see the key.
+    d, bs, P, C = 4, 4, 4, 4
+    q = np.zeros((1, C, 1, d), np.float32)
+    k = np.zeros((1, 1, P + C, d), np.float32)
+    q[0, 0, 0] = [1, 0, 0, 0]
+    q[0, 1, 0] = [0, 1, 0, 0]
+    q[0, 2, 0] = [0, 0, 1, 0]
+    q[0, 3, 0] = [0, 0, 0, 1]
+    k[0, 0, P + 3] = [50, 0, 0, 0]   # huge only against query 0, which is causally blind to it
+    k[0, 0, P + 0] = [0, 0, 0, 2]    # seen by every query; logit 2*0.5 = 1.0 with query 3
+    me = O.block_scores_exact(q, k, P, bs)
+    assert me[0, 0, 0, 1] == pytest.approx(1.0, abs=1e-12)   # max over causal pairs = q3.k(P+0)
+    mp = O.block_scores_pooled(q, k, P, bs)
+    assert mp[0, 0, 0, 1] == pytest.approx(50 * 0.25 * 0.5, abs=1e-12)  # qbar = 1/4 of each axis
+
+
 def test_constant_keys_keep_everything():
     # identical keys everywhere -> all in-causal scores equal -> all kept
     q, k, _ = random_qkv(1, 4, 1, 8, 16, 48, seed=2)
