@@ -9,16 +9,23 @@ paged attention over the tabled blocks, for the FINAL chunk of the workload (KV 
 
 Prints ONE JSON line (rank 0). value = attention ms per chunk (lower is better), inputs resident
 in HBM, L2 flushed before every timed step (a 512 MiB write), CUDA events on the launch stream,
-max over ranks. N > 1: KV-head groups are sharded over ranks (one KV group per GPU at N=8) and
-the per-rank head outputs are all-gathered each step (strong scaling: one chunk) -- by default
-inside the attention kernel (P2P stores into every rank's symmetric-memory buffer over NVLink + a
-signal barrier, cpa_chunk_step_peer); --collective nccl times NCCL all_gather_into_tensor instead.
+max over ranks. --gpus N > 1 without a torchrun environment re-launches itself under
+`torch.distributed.run --nproc-per-node N` (one rank per GPU, NCCL); under torchrun, WORLD_SIZE must
+equal --gpus. KV-head groups are sharded over the ranks (one KV group per GPU at N=8) and the per-rank
+head outputs are all-gathered each step (strong scaling: one chunk) -- by default inside the attention
+kernel (P2P stores into every rank's symmetric-memory buffer over NVLink + a signal barrier,
+cpa_chunk_step_peer); --collective nccl times NCCL all_gather_into_tensor instead.
+
+--impl reference runs the tier's reference arm: the fp64 CPU oracle (oracle/, as it stands) on the
+host cores, on the same workload and metric; the GPU arm's cpu_baseline is that arm on a bounded sample.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -51,12 +58,43 @@ def peaks():
         return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def bench_config(args, world):
+    """The `config` object of the JSON line: a function of the command line only, so the GPU arm and
+    the reference arm (same flags) print the same dict."""
+    cfg = CONFIGS[args.config]
+    P, C, L = cfg.chunk_geometry()
+    one_dev = os.environ.get("CPA_BENCH_ONE_DEVICE") == "1"
+    if world == 1:
+        par = "kv-group shard x1"
+    elif one_dev:
+        par = f"kv-group shard x{world} + gloo all-gather (single-device test mode)"
+    elif args.collective == "peer":
+        par = f"kv-group shard x{world} + fused peer-store all-gather (NVLink P2P, cpa_chunk_step_peer)"
+    else:
+        par = f"kv-group shard x{world} + nccl all-gather"
+    graph = not args.no_graph and not one_dev and (world == 1 or args.collective == "peer")
+    return {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk,
+            "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": cfg.head_dim,
+            "block_size": cfg.block_size, "alpha": ALPHA, "needle_density": RHO,
+            "exec_group_size": args.exec_group or cfg.group_size,
+            "scorer": "exact tile max (SPEC.md:223)" if args.exact_scores else "pooled query (SPEC.md:269)",
+            "parallelism": par, "l2": "flushed (512 MiB write) before every timed step",
+            "launch": "CUDA graph of the chunk step" if graph else "direct",
+            "v_cache_dtype": "f16" if args.v_f16 else "bf16"}
+
+
 # ------------------------------------------------------------------------------ algorithmic work
 def attention_flops(indptr, indices, C, P, bs, E, d):
     """4*d*E*sum over rows r of sum_p |A(p)| (exact causal pairs on the tabled blocks)."""
     L = P + C
     total = 0
-    p_last = P + C  # exclusive bound of absolute query positions
     for r in range(len(indptr) - 1):
         js = np.asarray(indices[indptr[r]:indptr[r + 1]], np.int64)
         lo = js * bs
@@ -135,39 +173,150 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------------------------ CPU oracle leg
-def cpu_oracle_sample(cfg, seed, q, k, v, P, C, budget_s=15.0):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the chunk step and extrapolate to
-    ms/chunk: estimator for 2 query heads + attention for sampled query rows (rows/heads are
-    independent, so the extrapolation is exact in work)."""
-    import oracle as O
+# ------------------------------------------------------------------------------ CPU oracle (reference arm)
+# The oracle as it stands, on every host core: one worker process per core (fork: the parent's inputs are
+# shared copy-on-write; BLAS limited to one thread per worker). Work unit = one execution group (b, g):
+# its estimator + threshold + unions + CSR row, then its attention rows in batches.
+_OR = {}
+
+
+def _or_init():
     try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
     except Exception:
-        threads = os.cpu_count()
-    bs, E = cfg.block_size, cfg.group_size
-    B, Hq = cfg.batch, cfg.num_q_heads
-    t0 = time.perf_counter()
-    heads = [0, 1]
-    m = O.block_scores_pooled(q[:, :, heads], k[:, :1], P, bs)
-    t_est = (time.perf_counter() - t0) / (len(heads) * B) * B * Hq
-    # tables of group 0 from the sampled heads' mask (the union is integer work; negligible)
-    M = O.threshold_mask(m, ALPHA, C, P, bs)
-    ip, ix = O.tables_from_mask(M, len(heads), P // bs)
-    rng = np.random.default_rng(0)
-    n_rows, t_attn = 0, 0.0
-    t1 = time.perf_counter()
-    while time.perf_counter() - t1 < budget_s and n_rows < 4096:
-        rows = [(0, int(rng.integers(C)), int(rng.integers(2))) for _ in range(16)]
-        O.paged_attention(q[:, :, :2], k[:, :1], v[:, :1], P, bs, ip, ix, E=2, rows=rows)
-        n_rows += len(rows)
-    t_attn = (time.perf_counter() - t1) / n_rows * B * C * Hq
-    total_ms = (t_est + t_attn) * 1e3
-    return {"value": total_ms, "unit": "ms/chunk", "cores": threads, "kind": "oracle",
-            "sample": f"fp64 numpy oracle: pooled estimator for {len(heads)} of {B * Hq} (b,h) heads + "
-                      f"attention for {n_rows} of {B * C * Hq} query rows, extrapolated linearly to the "
-                      f"whole {cfg.name} final chunk"}
+        pass
+
+
+def _or_group_slices(gi):
+    d = _OR
+    b, g = divmod(gi, d["Gn"])
+    kvh = (g * d["E"]) // d["E_kv"]
+    q = d["q"][b:b + 1, :, g * d["E"]:(g + 1) * d["E"]]
+    return q, d["k"][b:b + 1, kvh:kvh + 1], d["v"][b:b + 1, kvh:kvh + 1]
+
+
+def _or_tables(gi):
+    import oracle as O
+    d = _OR
+    q, k, _ = _or_group_slices(gi)
+    if d["exact"]:
+        m = O.block_scores_exact(q, k, d["P"], d["bs"])
+    else:
+        m = O.block_scores_pooled(q, k, d["P"], d["bs"])
+    M = O.threshold_mask(m, ALPHA, d["C"], d["P"], d["bs"])
+    return O.tables_from_mask(M, d["E"], d["P"] // d["bs"])
+
+
+def _or_rows(task):
+    import oracle as O
+    gi, ip, ix, rows = task
+    q, k, v = _or_group_slices(gi)
+    O.paged_attention(q, k, v, _OR["P"], _OR["bs"], ip, ix, E=_OR["E"], rows=rows)
+    return len(rows)
+
+
+def oracle_chunk(args, rows_per_group=None, log=None):
+    """Time the oracle on the final chunk of args.config: every group's estimator + tables, then the
+    attention rows (all of them, or `rows_per_group` evenly spaced query positions x all heads of each
+    group). Returns (ms/chunk, timed wall ms, description)."""
+    import multiprocessing as mp
+    cfg = CONFIGS[args.config]
+    seed = seed_of(args.config)
+    P, C, L = cfg.chunk_geometry()
+    E_kv = cfg.group_size
+    E = args.exec_group or E_kv
+    Gn = cfg.num_q_heads // E
+    t_gen = time.perf_counter()
+    k, v = make_kv(cfg, seed, RHO)
+    q = make_q(cfg, seed)
+    _OR.update(q=q, k=k, v=v, P=P, C=C, bs=cfg.block_size, E=E, E_kv=E_kv, Gn=Gn, exact=args.exact_scores)
+    cores = host_cores()
+    groups = cfg.batch * Gn
+    if rows_per_group is None or rows_per_group >= C * E:
+        ps = list(range(C))
+    else:
+        ps = sorted(set(np.linspace(0, C - 1, max(1, rows_per_group // E)).round().astype(int).tolist()))
+    rows_g = [(0, int(p), hl) for p in ps for hl in range(E)]
+    n_total = groups * C * E
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_or_init) as pool:
+        pool.map(int, range(cores))  # workers up before the clock starts
+        if log:
+            log(f"[oracle] inputs generated in {time.perf_counter() - t_gen:.1f} s; {cores} worker processes")
+        t0 = time.perf_counter()
+        tabs = pool.map(_or_tables, range(groups), chunksize=1)
+        t1 = time.perf_counter()
+        per = max(1, min(64, len(rows_g) // max(1, (2 * cores) // groups + 1)))
+        tasks = [(gi, tabs[gi][0], tabs[gi][1], rows_g[s:s + per]) for gi in range(groups)
+                 for s in range(0, len(rows_g), per)]
+        done = sum(pool.imap_unordered(_or_rows, tasks, chunksize=1))
+        t2 = time.perf_counter()
+    n_timed = done
+    t_est, t_att = (t1 - t0) * 1e3, (t2 - t1) * 1e3
+    ms = t_est + t_att * (n_total / n_timed)
+    if n_timed == n_total:
+        desc = (f"whole {cfg.name} final chunk: estimator + tables of all {groups} execution groups and "
+                f"attention for all {n_total} (b, p, h) query rows, fp64 numpy oracle, {cores} worker processes")
+    else:
+        desc = (f"estimator + tables of all {groups} execution groups (complete, {t_est:.0f} ms) + attention "
+                f"for {n_timed} of {n_total} (b, p, h) query rows ({len(ps)} evenly spaced query positions x "
+                f"all heads of every group, {t_att:.0f} ms), extrapolated linearly in rows; fp64 numpy oracle, "
+                f"{cores} worker processes")
+    return ms, (t2 - t0) * 1e3, desc, cores
+
+
+def run_reference(args):
+    """The tier's reference arm: the fp64 oracle as it stands on the host cores, same workload, metric
+    and config as the GPU arm. Rank 0 only (other torchrun ranks exit without work). One step = the
+    whole final chunk (no extrapolation) unless --oracle-rows-per-group samples it (cpu_baseline leg)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    log = lambda m: print(m, file=sys.stderr, flush=True)
+    vals, walls = [], []
+    n_steps = 1 if args.oracle_rows_per_group is None else max(1, args.steps)
+    for _ in range(n_steps):
+        ms, wall, desc, cores = oracle_chunk(args, args.oracle_rows_per_group, log)
+        vals.append(ms)
+        walls.append(wall)
+    val = float(np.mean(vals))
+    whole = args.oracle_rows_per_group is None
+    out = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": args.gpus,
+           "steps": n_steps, "warmup": 0, "ms_per_step": round(val, 2), "higher_is_better": False,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": bench_config(args, args.gpus),
+           "cpu_baseline": {"value": round(val, 2), "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": desc, "timed_wall_ms": round(float(np.mean(walls)), 1)},
+           "e2e": {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "note": ("steps = whole chunks actually timed (one chunk of the oracle takes minutes on the host "
+                    "cores, so --steps/--warmup are not repeated); warm-up = input generation + worker start-up"
+                    if whole else "bounded sample per step, extrapolated to ms/chunk (see cpu_baseline.sample)")}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_leg(args):
+    """The oracle on a bounded sample of the same chunk (the reference arm with
+    --oracle-rows-per-group), run in a child process: it forks one worker per core, which must not
+    happen in a process that holds a CUDA context."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", args.config,
+           "--oracle-rows-per-group", str(args.cpu_rows_per_group), "--steps", "1", "--gpus", str(args.gpus),
+           "--collective", args.collective]
+    if args.exact_scores:
+        cmd.append("--exact-scores")
+    if args.exec_group:
+        cmd += ["--exec-group", str(args.exec_group)]
+    if not args.v_f16:
+        cmd.append("--v-bf16")
+    if args.no_graph:
+        cmd.append("--no-graph")
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+        line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
+        return json.loads(line)["cpu_baseline"]
+    except Exception as ex:  # noqa: BLE001 -- reported, never fatal for the GPU arm
+        return {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+                "sample": f"failed: {type(ex).__name__}: {ex}"[:300]}
 
 
 # ------------------------------------------------------------------------------ GPU arm
@@ -209,7 +358,6 @@ def run_gpu(args):
     if one_dev:
         local = 0
     torch.cuda.set_device(local)
-    backend = "gloo" if one_dev else "nccl"
     # CPA_BENCH_PEER_W1=1 (test only, under torchrun --nproc-per-node 1): a 1-rank NCCL group so the
     # fused peer path runs through real symmetric memory on a single-GPU box.
     force_peer = os.environ.get("CPA_BENCH_PEER_W1") == "1" and world == 1
@@ -218,6 +366,9 @@ def run_gpu(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()  # eager communicator init (NCCL_DEBUG=INFO logs it on stderr)
+        print(f"[bench] rank {rank}/{world}: process group up ({dist.get_backend()}), cuda:{local}",
+              file=sys.stderr, flush=True)
 
     def max_over_ranks(vals):
         if world == 1:
@@ -237,36 +388,40 @@ def run_gpu(args):
     nkvb = -(-L // bs)
     pt, npages = page_layout(cfg.batch, nkvb, seed)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
-    vpool = dev(to_pool(v, pt, npages, bs))
-    if args.v_f16:  # CPA_F_V_F16: the V pool holds fp16 (exact for these bf16 values)
-        vpool = vpool.half()
-    cache = cpa.PagedKVCache(dev(to_pool(k, pt, npages, bs)), vpool, torch.from_numpy(pt).cuda())
+    kpool = dev(to_pool(k, pt, npages, bs))
+    vpool_bf16 = dev(to_pool(v, pt, npages, bs))
+    vpool = vpool_bf16.half() if args.v_f16 else vpool_bf16  # CPA_F_V_F16: fp16 pool (exact for these values)
+    ptab = torch.from_numpy(pt).cuda()
+    cache = cpa.PagedKVCache(kpool, vpool, ptab)
     dq = dev(q)
     kc = dev(k[:, :, P:].transpose(0, 2, 1, 3))  # the chunk's own K/V [B, C, Hkv, d] (re-appended)
     vc = dev(v[:, :, P:].transpose(0, 2, 1, 3))
+    del k, v
     E_exec = args.exec_group or E
     vflag = cpa.F_V_F16 if args.v_f16 else 0
+    sflag = cpa.F_EXACT_SCORES if args.exact_scores else 0
     p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
-                        flags=(cpa.F_EXACT_SCORES if args.exact_scores else 0) | vflag)
+                        flags=sflag | vflag)
     tables = cpa.alloc_tables(p)
     ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
     o = torch.empty(cfg.batch, C, hq_l, d, dtype=torch.bfloat16, device="cuda")
     o_all = torch.empty(world, cfg.batch, C, hq_l, d, dtype=torch.bfloat16, device="cuda")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     stream = torch.cuda.current_stream()
+    config = bench_config(args, world)
     # N > 1: the head-output all-gather is fused into the attention epilogue (P2P stores into every
     # rank's symmetric-memory buffer + a signal barrier, cpa_chunk_step_peer); NCCL all-gather after a
     # local step is the baseline (--collective nccl) and the fallback if symmetric memory is unavailable.
-    collective = "none" if world == 1 and not force_peer else ("gloo all-gather" if one_dev else args.collective)
     peers = None
-    if collective == "peer":
+    full_shape = (cfg.batch, C, cfg.num_q_heads, d)
+    if (world > 1 or force_peer) and not one_dev and args.collective == "peer":
         try:
-            peers, o_gathered = peer_setup(torch, dist, cpa, (cfg.batch, C, cfg.num_q_heads, d), world, rank)
-            collective = "fused peer-store all-gather (NVLink P2P, cpa_chunk_step_peer)"
+            peers, o_gathered = peer_setup(torch, dist, cpa, full_shape, world, rank)
         except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
-            collective = f"nccl all-gather (symmetric memory unavailable: {type(ex).__name__}: {ex})"[:200]
-    elif collective == "nccl":
-        collective = "nccl all-gather"
+            config["parallelism"] = (f"kv-group shard x{world} + nccl all-gather (fallback: symmetric memory "
+                                     f"unavailable: {type(ex).__name__}: {ex})")[:240]
+            config["launch"] = "direct"
+    use_graph = config["launch"].startswith("CUDA graph")
 
     def step():
         if peers is not None:
@@ -278,37 +433,37 @@ def run_gpu(args):
 
     # The timed step is one replay of a CUDA graph of the whole chunk step (append, estimator, tables,
     # attention [, fused all-gather + barrier]): the C ABI is stream-ordered, never allocates or syncs,
-    # so it captures as is; replays drop the per-kernel launch gaps (8% of the step at one KV group per
-    # GPU). NCCL / gloo all-gather modes run directly.
-    launch = "direct"
+    # so it captures as is; replays drop the per-kernel launch gaps. Event nodes captured around the
+    # attention kernel time it inside every timed step (roofline). NCCL / gloo all-gather modes run directly.
     step()  # one direct step: kernels per step for gpu_launches
     launches_per_step = cpa.last_launch_count()
-    att_ev = None  # attention-kernel events inside the timed steps (roofline timing)
-    if not args.no_graph and not one_dev and (world == 1 or peers is not None):
+    att_ev = None
+
+    def capture(p_, cache_):
+        ev = (torch.cuda.Event(enable_timing=True, external=True),
+              torch.cuda.Event(enable_timing=True, external=True))
+        g = torch.cuda.CUDAGraph()
+        # thread_local: the NCCL watchdog thread may query events while this thread captures
+        with torch.cuda.graph(g, capture_error_mode="thread_local"):
+            # == cpa_chunk_step(_peer): append + build_tables + attention (same workspace, same stream)
+            cpa.append_kv(p_, kc, vc, cache_)
+            cpa.build_tables(p_, dq, cache_, tables, workspace=ws)
+            ev[0].record()
+            if peers is not None:
+                cpa.paged_attention_peer(p_, dq, cache_, tables, peers, workspace=ws)
+            else:
+                cpa.paged_attention(p_, dq, cache_, tables, o, workspace=ws)
+            ev[1].record()
+        return g, ev
+
+    if use_graph:
         step()
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        # thread_local: the NCCL watchdog thread may query events while this thread captures
-        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
-            if peers is None:
-                # cpa_chunk_step == append + build_tables + paged_attention (same workspace, same stream);
-                # split here so that event nodes bracket the attention kernel inside every timed step
-                att_ev = (torch.cuda.Event(enable_timing=True, external=True),
-                          torch.cuda.Event(enable_timing=True, external=True))
-                cpa.append_kv(p, kc, vc, cache)
-                cpa.build_tables(p, dq, cache, tables, workspace=ws)
-                att_ev[0].record()
-                cpa.paged_attention(p, dq, cache, tables, o, workspace=ws)
-                att_ev[1].record()
-            else:
-                step()
+        graph, att_ev = capture(p, cache)
         torch.cuda.synchronize()
         step = graph.replay
-        launch = "CUDA graph of the chunk step"
 
-    att_in_step = []
-
-    def timed(fn, iters, warm, inner=None):
+    def timed(fn, iters, warm, inner=None, ev=None):
         for _ in range(warm):
             fn()
         torch.cuda.synchronize()
@@ -322,17 +477,18 @@ def run_gpu(args):
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
             if inner is not None:
-                inner.append(att_ev[0].elapsed_time(att_ev[1]))
+                inner.append(ev[0].elapsed_time(ev[1]))
         return ts
 
     # ---- headline: W warm-up steps, K timed steps, barrier + sync on both sides
+    att_in_step = []
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     with ClockSampler(local) as clk:
-        ts = timed(step, args.steps, 0, att_in_step if att_ev is not None else None)
+        ts = timed(step, args.steps, 0, att_in_step if att_ev is not None else None, att_ev)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -340,13 +496,10 @@ def run_gpu(args):
     if peers is not None and int(peers.dev_status.item()) != 0:
         raise RuntimeError(f"rank {rank}: peer barrier timed out waiting for rank {int(peers.dev_status.item()) - 1}")
 
-    # ---- stage breakdown and the dense baseline (same kernels, tables = all blocks)
+    # ---- stage breakdown and the dense baseline (same kernels, tables = all blocks), rank-local
     reps = max(3, min(args.steps, 10))
     t_tables = float(np.mean(timed(lambda: cpa.build_tables(p, dq, cache, tables, workspace=ws), reps, 1)))
-    t_attn = timed(lambda: cpa.paged_attention(p, dq, cache, tables, o, workspace=ws), reps, 1)
-    t_attn = float(np.mean(t_attn))
-    # roofline: the attention kernel's duration inside the timed steps (graph event nodes around it)
-    # when available, else its separately timed launches
+    t_attn = float(np.mean(timed(lambda: cpa.paged_attention(p, dq, cache, tables, o, workspace=ws), reps, 1)))
     t_attn_roof, roof_timing = t_attn, "separate launches (CUDA events, L2 flushed)"
     if att_in_step:
         t_attn_roof = float(np.mean(att_in_step))
@@ -362,11 +515,25 @@ def run_gpu(args):
     density = (ip[-1] - cfg.batch * Gx * (nkvb - P // bs)) / (cfg.batch * Gx * (P // bs))
     # per-stage sparsity from the GPU's own mask bits (one extra build, outside the timed region)
     pm = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
-                         flags=cpa.F_MASK_OUT | (cpa.F_EXACT_SCORES if args.exact_scores else 0) | vflag)
+                         flags=cpa.F_MASK_OUT | sflag | vflag)
     tm = cpa.alloc_tables(pm, mask=True)
     cpa.build_tables(pm, dq, cache, tm)
     nqb = -(-C // bs)
     sparsity = sparsity_report(tm.mask_bits.cpu().numpy(), nkvb, P // bs, nqb, hq_l, E_exec, E)
+
+    # ---- the same step with the other V pool dtype (bf16 pool: V converted per page in the kernel)
+    other_pool = None
+    if use_graph and peers is None:
+        p_o = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
+                              flags=sflag | (0 if args.v_f16 else cpa.F_V_F16))
+        cache_o = cpa.PagedKVCache(kpool, vpool_bf16 if args.v_f16 else vpool_bf16.half(), ptab)
+        cpa.chunk_step(p_o, dq, cache_o, tables, o, kc, vc, workspace=ws)
+        torch.cuda.synchronize()
+        g_o, _ = capture(p_o, cache_o)
+        t_o = float(np.mean(timed(g_o.replay, args.steps, 2)))
+        other_pool = {"v_cache_dtype": "bf16" if args.v_f16 else "f16", "ms_per_chunk": round(t_o, 4)}
+        del g_o, cache_o
+        cpa.chunk_step(p, dq, cache, tables, o, kc, vc, workspace=ws)  # restore this arm's pool contents
 
     # ---- e2e: the same step through the public API with HOST buffers (pinned), copies timed
     hq_pin = dq.cpu().pin_memory()
@@ -389,28 +556,44 @@ def run_gpu(args):
 
     e2e_serial_ms = float(np.mean(timed(e2e_step, args.steps, 1)))
     e2e_ms, e2e_mode = e2e_serial_ms, "serial: H2D, chunk step, D2H in stream order, per step"
-    if world == 1:
+    if world == 1 or peers is not None:
         # the same public API fed from pinned host buffers as a serving loop would: HostChunkStream
         # overlaps step i+1's H2D and step i-1's D2H with step i's kernels; the timed region spans all
-        # K steps (first H2D to last D2H, CUDA events), every copy inside it.
+        # K steps (first H2D to last D2H, CUDA events), every copy inside it. N > 1: one symmetric-memory
+        # gathered buffer per staging slot (three slots, see HostChunkStream).
+        hp, hg = None, None
+        if peers is not None:
+            hp, hg = [peers], [o_gathered]
+            for _ in range(2):
+                pr, gb = peer_setup(torch, dist, cpa, full_shape, world, rank)
+                hp.append(pr)
+                hg.append(gb)
         runner = cpa.HostChunkStream(p, cache, tables, tuple(dq.shape), tuple(kc.shape), workspace=ws,
-                                     graphs=not args.no_graph)
-        outs = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for _ in range(2)]
-        for i in range(max(2, args.warmup)):
-            runner.submit(hq_pin, outs[i & 1], hk_pin, hv_pin)
+                                     graphs=use_graph, peers=hp, gathered=hg, rank=rank)
+        outs = [torch.empty(o.shape, dtype=o.dtype).pin_memory() for _ in range(runner.n)]
+        for i in range(max(runner.n, args.warmup)):
+            runner.submit(hq_pin, outs[i % runner.n], hk_pin, hv_pin)
         runner.synchronize()
+        if world > 1:
+            dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(runner.s_in)
         for i in range(args.steps):
-            runner.submit(hq_pin, outs[i & 1], hk_pin, hv_pin)
+            runner.submit(hq_pin, outs[i % runner.n], hk_pin, hv_pin)
         b.record(runner.s_out)
         runner.synchronize()
         e2e_ms = a.elapsed_time(b) / args.steps
         e2e_mode = ("pipelined (HostChunkStream: H2D of step i+1 and D2H of step i-1 overlap step i), "
-                    "K steps timed first H2D to last D2H; each step streams > L2 (268 MB of K pages)")
+                    "K steps timed first H2D to last D2H; each step streams > L2 (the K pages)")
     h2d = (dq.numel() + kc.numel() + vc.numel()) * 2
     d2h = o.numel() * 2
-    e2e_ms, e2e_serial_ms, t_attn, t_dense, t_tables = max_over_ranks([e2e_ms, e2e_serial_ms, t_attn, t_dense, t_tables])
+    e2e_ms, e2e_serial_ms, t_attn, t_attn_roof, t_dense, t_tables, t_append = max_over_ranks(
+        [e2e_ms, e2e_serial_ms, t_attn, t_attn_roof, t_dense, t_tables, t_append])
+    # algorithmic FLOPs of the whole job's attention launches (sum over ranks) / the slowest rank's time
+    if world > 1:
+        tf = torch.tensor([float(f_sel), float(f_dense)], dtype=torch.float64, device="cpu" if one_dev else "cuda")
+        dist.all_reduce(tf)
+        f_sel, f_dense = int(tf[0].item()), int(tf[1].item())
 
     peak_tf, peak_bw, peak_src = peaks()
     achieved_tf = f_sel / (t_attn_roof * 1e-3) / 1e12
@@ -422,35 +605,30 @@ def run_gpu(args):
     except Exception:
         pass
 
-    out = None
+    cpu = cpu_baseline_leg(args) if rank == 0 else None
     if rank == 0:
-        cpu = cpu_oracle_sample(cfg, seed, q, k, v, P, C, budget_s=args.cpu_budget) if world == 1 else None
         out = {
             "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk,
-                       "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": d,
-                       "block_size": bs, "alpha": ALPHA, "needle_density": RHO, "exec_group_size": E_exec,
-                       "scorer": "exact tile max (SPEC.md:223)" if args.exact_scores else "pooled query (SPEC.md:269)",
-                       "parallelism": f"kv-group shard x{world}" + (f" + {collective}" if collective != "none" else ""),
-                       "l2": "flushed (512 MiB write) before every timed step", "launch": launch,
-                       "v_cache_dtype": "f16" if args.v_f16 else "bf16"},
+            "config": config,
             "dense_ms_per_chunk": round(t_dense, 4),
             "speedup_vs_dense": round(t_dense / ms, 3),
             "attention_only_speedup": round(t_dense / t_attn, 3),
             "stage_ms": {"append": round(t_append, 4), "estimator+tables": round(t_tables, 4),
                          "attention": round(t_attn, 4)},
+            "other_v_pool": other_pool,
             "tabled_prefix_density": round(float(density), 4),
             "sparsity": sparsity,
             "effective_tflops": round(f_dense / (ms * 1e-3) / 1e12, 1),
-            "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf,
-                         "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4), "traffic": traffic,
-                         "kernel": "k_paged_attn", "peak_source": peak_src, "timing": roof_timing,
-                         "algorithmic_flops_per_launch": f_sel},
+            "roofline": {"bound": "tensor", "achieved": round(achieved_tf, 1), "peak": peak_tf * world,
+                         "unit": "TFLOP/s", "frac": round(achieved_tf / (peak_tf * world), 4), "traffic": traffic,
+                         "kernel": "k_paged_attn_2cta", "peak_source": peak_src + (f" x {world} GPUs" if world > 1 else ""),
+                         "timing": roof_timing, "algorithmic_flops_per_launch": f_sel},
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "mode": e2e_mode, "serial_value": round(e2e_serial_ms, 4)},
+                    "mode": e2e_mode, "serial_value": round(e2e_serial_ms, 4),
+                    "bytes_note": "per rank" if world > 1 else "whole job"},
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
             "paper_context": "2.72x attention speedup at 128K on 2xH200 (TP=2, B=8, chunk 1024; PAPER.md:612, 620)",
@@ -461,33 +639,24 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
-# ------------------------------------------------------------------------------ reference arm
-def run_reference(args):
-    """The oracle as it stands on the host cores (the tier's reference arm)."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    cfg = CONFIGS[args.config]
-    seed = seed_of(args.config)
-    P, C, L = cfg.chunk_geometry()
-    k, v = make_kv(cfg, seed, RHO, kv_heads=range(0, 1))
-    q = make_q(cfg, seed, q_heads=range(0, cfg.group_size))
-    qf = np.zeros((cfg.batch, C, cfg.num_q_heads, cfg.head_dim), np.float32)
-    qf[:, :, :cfg.group_size] = q
-    budget = max(2.0, 120.0 / max(1, args.steps + args.warmup))
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(cfg, seed, qf, k, v, P, C, budget_s=budget)
-        if i >= args.warmup:
-            vals.append(r["value"])
-    val = float(np.mean(vals))
-    out = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": 1,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(val, 2), "higher_is_better": False,
-           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk},
-           "cpu_baseline": {**r, "value": round(val, 2)},
-           "e2e": {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+# ------------------------------------------------------------------------------ launcher
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run, one rank per GPU
+    (the driver's own invocation is torchrun; both end up here with WORLD_SIZE == N)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")           # communicator init lines (nRanks) for the record
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout = the JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -500,7 +669,10 @@ def main():
     ap.add_argument("--exact-scores", action="store_true", help="NEXT-1: SPEC's exact tile-max scorer")
     ap.add_argument("--exec-group", type=int, default=0,
                     help="execution-group size E (0 = full KV group; 4 = sub-KV-group union, PAPER.md:498)")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-rows-per-group", type=int, default=256,
+                    help="cpu_baseline leg: oracle attention rows timed per execution group (extrapolated)")
+    ap.add_argument("--oracle-rows-per-group", type=int, default=None,
+                    help="reference arm: sample this many rows per group instead of the whole chunk")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph")
     ap.add_argument("--v-bf16", dest="v_f16", action="store_false",
                     help="keep the V pool in bf16 (converted per page inside the attention kernel) instead of the "
@@ -510,9 +682,30 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_gpu(args)
+        return 0
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        return launch_ranks(args)
+    if ws is not None and int(ws) != args.gpus:
+        print(f"[bench] refusing to run: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr, flush=True)
+        return 2
+    if os.environ.get("CPA_BENCH_LAUNCH_PROBE") == "1":  # test only (CPU): the launcher's rank wiring
+        import torch
+        import torch.distributed as dist
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        if world > 1:
+            dist.init_process_group("gloo")
+        t = torch.ones(1)
+        if world > 1:
+            dist.all_reduce(t)
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"n_gpus": world, "ranks_seen": int(t.item())}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    run_gpu(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

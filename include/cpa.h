@@ -225,6 +225,14 @@ CPA_API int cpa_chunk_step_peer(const cpa_params* p, const void* q, const void* 
                                 const cpa_kv_cache* cache, cpa_tables* tables, const cpa_peer_out* peers,
                                 void* ws, size_t ws_bytes, void* stream);
 
+/* The attention stage alone with the fused all-gather: cpa_paged_attention over `tables` (NULL =>
+ * dense) whose epilogue writes every peer_out[w] at this rank's head slice, then the barrier; i.e. the
+ * last two stages of cpa_chunk_step_peer, for callers that run append / cpa_build_tables separately
+ * (bench.py times the attention kernel inside the step this way). Errors as cpa_chunk_step_peer. */
+CPA_API int cpa_paged_attention_peer(const cpa_params* p, const void* q, const cpa_kv_cache* cache,
+                                     const cpa_tables* tables, const cpa_peer_out* peers, void* ws,
+                                     size_t ws_bytes, void* stream);
+
 /* The barrier alone (signal every peer with `epoch`, wait for all); peer_out is not used. */
 CPA_API int cpa_peer_barrier(const cpa_peer_out* peers, void* stream);
 

@@ -18,7 +18,7 @@ __all__ = [
     "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
     "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
     "paged_attention_copy", "block_sparse_attention", "expand_tables", "PeerOut", "chunk_step_peer",
-    "peer_barrier", "HostChunkStream",
+    "paged_attention_peer", "peer_barrier", "HostChunkStream",
     "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "F_NO_PERSIST", "F_PERSIST", "F_V_F16", "EXPORTED_SYMBOLS",
 ]
 
@@ -32,7 +32,7 @@ STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA
 EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",
                     "cpa_append_kv", "cpa_copy_workspace_bytes", "cpa_paged_attention_copy",
                     "cpa_block_sparse_attention", "cpa_expand_tables", "cpa_chunk_step_peer",
-                    "cpa_peer_barrier", "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
+                    "cpa_paged_attention_peer", "cpa_peer_barrier", "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
 
 
 class CpaError(RuntimeError):
@@ -100,8 +100,11 @@ def lib() -> ctypes.CDLL:
         L.cpa_chunk_step_peer.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(_Cache),
                                           ctypes.POINTER(_Tables), ctypes.POINTER(_PeerOut), vp, ctypes.c_size_t, vp]
         L.cpa_peer_barrier.argtypes = [ctypes.POINTER(_PeerOut), vp]
+        L.cpa_paged_attention_peer.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache),
+                                               ctypes.POINTER(_Tables), ctypes.POINTER(_PeerOut), vp,
+                                               ctypes.c_size_t, vp]
         for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv,
-                  L.cpa_chunk_step_peer, L.cpa_peer_barrier):
+                  L.cpa_chunk_step_peer, L.cpa_peer_barrier, L.cpa_paged_attention_peer):
             f.restype = i32
         L.cpa_status_string.argtypes = [i32]
         L.cpa_status_string.restype = ctypes.c_char_p
@@ -157,13 +160,25 @@ class PagedKVCache:
     page_table: torch.Tensor
     page_stride: int = 0
     head_stride: int = 0
+    num_pages: int = 0  # 0 => k_pages.shape[0] (only valid for the default [pages, Hkv, bs, d] pool)
 
     def _c(self) -> _Cache:
         assert self.k_pages.dtype == torch.bfloat16 and self.v_pages.dtype in (torch.bfloat16, torch.float16)
         assert self.page_table.dtype == torch.int32 and self.page_table.is_contiguous()
-        num_pages = self.k_pages.shape[0]
+        if self.num_pages:
+            num_pages = self.num_pages
+        elif self.page_stride == 0 and self.head_stride == 0:
+            num_pages = self.k_pages.shape[0]
+        else:
+            raise ValueError("PagedKVCache with explicit strides needs num_pages (the page index range of the pool)")
         return _Cache(_ptr(self.k_pages), _ptr(self.v_pages), self.page_stride, self.head_stride,
                       _ptr(self.page_table), self.page_table.shape[-1], num_pages)
+
+    def _check_v(self, p: "Params"):
+        """The V pool dtype must match CPA_F_V_F16 (fp16 pool <=> flag), else results are garbage."""
+        if (self.v_pages.dtype == torch.float16) != bool(p.flags & F_V_F16):
+            raise ValueError(f"v_pages dtype {self.v_pages.dtype} does not match CPA_F_V_F16 "
+                             f"({'set' if p.flags & F_V_F16 else 'unset'})")
 
 
 @dataclass
@@ -218,6 +233,7 @@ def build_tables(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockT
 def paged_attention(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: Optional[BlockTables],
                     out: torch.Tensor, workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     ws = _ws(p, workspace, q.device, stream)
+    cache._check_v(p)
     c = cache._c()
     t = tables._c() if tables is not None else None
     _check(lib().cpa_paged_attention(ctypes.byref(p), _ptr(q), ctypes.byref(c),
@@ -230,6 +246,7 @@ def chunk_step(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTab
                k_chunk: Optional[torch.Tensor] = None, v_chunk: Optional[torch.Tensor] = None,
                workspace: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     ws = _ws(p, workspace, q.device, stream)
+    cache._check_v(p)
     c, t = cache._c(), tables._c()
     _check(lib().cpa_chunk_step(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
                                 ctypes.byref(t), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
@@ -260,9 +277,22 @@ def chunk_step_peer(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: Blo
                     workspace: Optional[torch.Tensor] = None, stream=None) -> None:
     """cpa_chunk_step with the head-output all-gather fused into the attention epilogue (cpa.h)."""
     ws = _ws(p, workspace, q.device, stream)
+    cache._check_v(p)
     c, t, pr = cache._c(), tables._c(), peers._next()
     _check(lib().cpa_chunk_step_peer(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
                                      ctypes.byref(t), ctypes.byref(pr), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def paged_attention_peer(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: Optional[BlockTables],
+                         peers: PeerOut, workspace: Optional[torch.Tensor] = None, stream=None) -> None:
+    """cpa_paged_attention with the fused head-output all-gather + barrier (cpa.h)."""
+    ws = _ws(p, workspace, q.device, stream)
+    cache._check_v(p)
+    c, pr = cache._c(), peers._next()
+    t = tables._c() if tables is not None else None
+    _check(lib().cpa_paged_attention_peer(ctypes.byref(p), _ptr(q), ctypes.byref(c),
+                                          ctypes.byref(t) if t is not None else None, ctypes.byref(pr), _ptr(ws),
+                                          ws.numel(), _stream(stream)))
 
 
 def peer_barrier(peers: PeerOut, stream=None) -> None:
@@ -271,6 +301,7 @@ def peer_barrier(peers: PeerOut, stream=None) -> None:
 
 
 def append_kv(p: Params, k_chunk: torch.Tensor, v_chunk: torch.Tensor, cache: PagedKVCache, stream=None):
+    cache._check_v(p)
     c = cache._c()
     _check(lib().cpa_append_kv(ctypes.byref(p), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c), _stream(stream)))
 
@@ -281,6 +312,7 @@ def paged_attention_copy(p: Params, q: torch.Tensor, cache: PagedKVCache, tables
     need = int(lib().cpa_copy_workspace_bytes(ctypes.byref(p)))
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=q.device)
+    cache._check_v(p)
     c, t = cache._c(), tables._c()
     _check(lib().cpa_paged_attention_copy(ctypes.byref(p), _ptr(q), ctypes.byref(c), ctypes.byref(t), _ptr(out),
                                           _ptr(workspace), workspace.numel(), _stream(stream)))
@@ -290,6 +322,7 @@ def paged_attention_copy(p: Params, q: torch.Tensor, cache: PagedKVCache, tables
 def block_sparse_attention(p: Params, q: torch.Tensor, cache: PagedKVCache, mask_bits: torch.Tensor,
                            out: torch.Tensor, stream=None) -> torch.Tensor:
     """NEXT-3 ablation: execute a 2D per-(b,h,q-block) mask [B,Hq,nqb,nwords] directly (see cpa.h)."""
+    cache._check_v(p)
     c = cache._c()
     _check(lib().cpa_block_sparse_attention(ctypes.byref(p), _ptr(q), ctypes.byref(c), _ptr(mask_bits), _ptr(out),
                                             None, 0, _stream(stream)))
@@ -306,46 +339,67 @@ def expand_tables(p: Params, tables: BlockTables, mask_bits: torch.Tensor, strea
 class HostChunkStream:
     """Chunk steps fed from pinned HOST buffers, pipelined over three streams: the H2D copy of step
     i+1's inputs and the D2H copy of step i-1's output overlap step i's kernels (device staging is
-    double-buffered; the cache, tables and workspace are used in stream order on the compute stream).
+    multi-buffered; the cache, tables and workspace are used in stream order on the compute stream).
     Plumbing only -- every step runs cpa_chunk_step (with graphs=True replayed from one captured CUDA
-    graph per staging slot). Read a host output only after synchronize()."""
+    graph per staging slot). Read a host output only after synchronize().
+
+    Multi-GPU (peers = one PeerOut per slot, gathered = this rank's gathered buffer [B, C, W*Hq, d] of
+    each slot): every step runs cpa_chunk_step_peer into its slot's gathered buffers on every rank, and
+    the D2H reads this rank's head slice. Three slots, and step i starts only after this rank's D2H of
+    step i-2 finished: any rank writing slot (i+1) % 3 at step i+1 has passed barrier i, so every rank
+    has finished its D2H of step i-2 == the last reader of that slot (cpa.h reuse rule)."""
 
     def __init__(self, p: Params, cache: PagedKVCache, tables: BlockTables, q_shape, kv_shape,
-                 workspace: Optional[torch.Tensor] = None, device="cuda", graphs: bool = False):
+                 workspace: Optional[torch.Tensor] = None, device="cuda", graphs: bool = False,
+                 peers=None, gathered=None, rank: int = 0):
         self.p, self.cache, self.tables = p, cache, tables
         self.ws = workspace if workspace is not None else _ws(p, None, device)
+        self.peers, self.gathered, self.rank = peers, gathered, rank
+        self.n = 3 if peers is not None else 2
+        if peers is not None:
+            assert gathered is not None and len(peers) == self.n and len(gathered) == self.n
         bf = torch.bfloat16
         o_dtype = torch.float32 if p.flags & F_OUT_F32 else bf
-        self.q = [torch.empty(q_shape, dtype=bf, device=device) for _ in range(2)]
-        self.k = [torch.empty(kv_shape, dtype=bf, device=device) for _ in range(2)]
-        self.v = [torch.empty(kv_shape, dtype=bf, device=device) for _ in range(2)]
-        self.o = [torch.empty(q_shape, dtype=o_dtype, device=device) for _ in range(2)]
+        self.q = [torch.empty(q_shape, dtype=bf, device=device) for _ in range(self.n)]
+        self.k = [torch.empty(kv_shape, dtype=bf, device=device) for _ in range(self.n)]
+        self.v = [torch.empty(kv_shape, dtype=bf, device=device) for _ in range(self.n)]
+        if peers is None:
+            self.o = [torch.empty(q_shape, dtype=o_dtype, device=device) for _ in range(self.n)]
+        else:
+            hq = q_shape[2]
+            self.o = [g[:, :, rank * hq:(rank + 1) * hq] for g in gathered]
         self.s_in, self.s_comp, self.s_out = (torch.cuda.Stream(device) for _ in range(3))
-        self.ev_in = [torch.cuda.Event() for _ in range(2)]
-        self.ev_comp = [torch.cuda.Event() for _ in range(2)]
-        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.ev_in = [torch.cuda.Event() for _ in range(self.n)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(self.n)]
+        self.ev_out = [torch.cuda.Event() for _ in range(self.n)]
         self.i = 0
         self.graphs = None
         if graphs:  # one graph per slot: append + estimator + tables + attention on that slot's buffers
             self.graphs = []
-            for s in range(2):
-                step = lambda s=s: chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s], self.k[s],
-                                              self.v[s], workspace=self.ws)
+            for s in range(self.n):
                 with torch.cuda.stream(self.s_comp):
                     for _ in range(2):
-                        step()
+                        self._step(s)
                 self.s_comp.synchronize()
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=self.s_comp):
-                    step()
+                    self._step(s)
                 self.graphs.append(g)
             torch.cuda.synchronize()
+
+    def _step(self, s: int, with_kv: bool = True, stream=None):
+        k, v = (self.k[s], self.v[s]) if with_kv else (None, None)
+        if self.peers is not None:
+            chunk_step_peer(self.p, self.q[s], self.cache, self.tables, self.peers[s], k, v, workspace=self.ws,
+                            stream=stream)
+        else:
+            chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s], k, v, workspace=self.ws, stream=stream)
 
     def submit(self, hq: torch.Tensor, ho: torch.Tensor, hk: Optional[torch.Tensor] = None,
                hv: Optional[torch.Tensor] = None) -> None:
         """Enqueue one chunk step: hq [B,C,Hq,d] (+ hk/hv [B,C,Hkv,d] to append) -> ho [B,C,Hq,d]."""
-        s = self.i & 1
-        self.s_in.wait_event(self.ev_comp[s])        # step i-2 has finished reading this slot
+        s = self.i % self.n
+        self.s_in.wait_event(self.ev_comp[s])        # step i-n has finished reading this slot
         with torch.cuda.stream(self.s_in):
             self.q[s].copy_(hq, non_blocking=True)
             if hk is not None:
@@ -353,15 +407,15 @@ class HostChunkStream:
                 self.v[s].copy_(hv, non_blocking=True)
             self.ev_in[s].record(self.s_in)
         self.s_comp.wait_event(self.ev_in[s])
-        self.s_comp.wait_event(self.ev_out[s])       # D2H of step i-2 has finished reading o[s]
+        self.s_comp.wait_event(self.ev_out[s])       # D2H of step i-n has finished reading o[s]
+        if self.peers is not None and self.i >= 2:
+            self.s_comp.wait_event(self.ev_out[(self.i - 2) % self.n])  # cross-rank slot reuse (class doc)
         if self.graphs is not None:  # the captured step always appends the slot's K/V
             assert hk is not None, "graphs=True runs the step with the chunk's K/V"
             with torch.cuda.stream(self.s_comp):
                 self.graphs[s].replay()
         else:
-            chunk_step(self.p, self.q[s], self.cache, self.tables, self.o[s],
-                       self.k[s] if hk is not None else None, self.v[s] if hk is not None else None,
-                       workspace=self.ws, stream=self.s_comp)
+            self._step(s, hk is not None, stream=self.s_comp)
         self.ev_comp[s].record(self.s_comp)
         self.s_out.wait_event(self.ev_comp[s])
         with torch.cuda.stream(self.s_out):

@@ -33,7 +33,7 @@ cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap
                                         const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st,
                                         int* launches);
 cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g,
-                          long long page_stride, long long head_stride, cudaStream_t st, int* launches);
+                          long long page_stride, long long head_stride, int num_sms, cudaStream_t st, int* launches);
 cudaError_t launch_gather_pages(const cpa_kv_cache& c, const int32_t* indptr, const int32_t* indices, const Geo& g,
                                 long long ps, long long hs, void* ck, void* cv, int32_t* cpt, cudaStream_t st,
                                 int* launches);
@@ -276,61 +276,85 @@ int kv_map(CUtensorMap* m, const void* pages, const Geo& g, int num_pages, long 
   return make_map(m, pages, 4, dims, str, box, what);
 }
 
-int build_tables_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c,
-                      long long ps, long long hs, cpa_tables* out, void* ws, size_t ws_bytes,
-                      cudaStream_t st, int num_sms) {
+// ---------------------------------------------------------------- plans
+// Every entry point validates and encodes its TMA descriptors (prep_*) BEFORE the first launch, so a
+// synchronous validation error leaves every output (pages, tables, o) untouched (cpa.h conventions).
+struct TablesPlan {
+  CUtensorMap tq, tk, tqq;
+  WS w;
+  float* scores;
+  bool mask_in, exact, scores_out;
+  const void* q;
+  const int32_t* page_table;
+  cpa_tables t;
+  int num_sms;
+};
+
+int prep_tables(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
+                long long hs, const cpa_tables* out, void* ws, size_t ws_bytes, int num_sms, TablesPlan* tp) {
   if (!out || !out->kv_indptr || !out->kv_indices) return fail(CPA_ERR_NULL, "tables pointers");
   if (out->capacity < (long long)g.B * g.Gn * g.nkvb)
     return fail(CPA_ERR_CAPACITY, "capacity %lld < B*Gn*nkvb = %lld", (long long)out->capacity,
                 (long long)g.B * g.Gn * g.nkvb);
-  const bool mask_in = (p->flags & CPA_F_MASK_IN) != 0;
-  if (mask_in && !out->mask_bits) return fail(CPA_ERR_NULL, "CPA_F_MASK_IN needs tables->mask_bits");
+  tp->mask_in = (p->flags & CPA_F_MASK_IN) != 0;
+  tp->exact = (p->flags & CPA_F_EXACT_SCORES) != 0;
+  tp->scores_out = (p->flags & CPA_F_SCORES_OUT) != 0;
+  if (tp->mask_in && !out->mask_bits) return fail(CPA_ERR_NULL, "CPA_F_MASK_IN needs tables->mask_bits");
   if ((p->flags & CPA_F_MASK_OUT) && !out->mask_bits) return fail(CPA_ERR_NULL, "CPA_F_MASK_OUT needs mask_bits");
-  if ((p->flags & CPA_F_SCORES_OUT) && (!out->scores || !out->row_max))
+  if (tp->scores_out && (!out->scores || !out->row_max))
     return fail(CPA_ERR_NULL, "CPA_F_SCORES_OUT needs scores and row_max");
-  WS w = carve(g, ws);
-  if (!ws || ws_bytes < w.total) return fail(CPA_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, w.total);
-  cudaError_t e;
-  int* launches = &g_launches;
-  float* scores = (p->flags & CPA_F_SCORES_OUT) ? out->scores : w.scores;
-  if (!mask_in) {
+  tp->w = carve(g, ws);
+  if (!ws || ws_bytes < tp->w.total) return fail(CPA_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, tp->w.total);
+  tp->scores = tp->scores_out ? out->scores : tp->w.scores;
+  tp->q = q;
+  tp->page_table = c->page_table;
+  tp->t = *out;
+  tp->num_sms = num_sms;
+  if (!tp->mask_in) {
     if (!q) return fail(CPA_ERR_NULL, "q is NULL");
     if (!aligned16(q)) return fail(CPA_ERR_MISALIGNED, "q not 16B aligned");
-    CUtensorMap tq, tk;
     cuuint64_t dims[2] = {(cuuint64_t)g.d, (cuuint64_t)2 * g.B * g.Gn * g.Rpad};
     cuuint64_t str[1] = {(cuuint64_t)g.d * 2};
     cuuint32_t box[2] = {64, 128};
     int s;
-    if ((s = make_map(&tq, w.qbar, 2, dims, str, box, "qbar")) != CPA_OK) return s;
-    if ((s = kv_map(&tk, c->k_pages, g, c->num_pages, ps, hs, "k")) != CPA_OK) return s;
-    if (p->flags & CPA_F_EXACT_SCORES) {  // NEXT-1: SPEC's exact tile-max scorer (full QK^T)
-      CUtensorMap tqq;
-      if ((s = q_map(&tqq, q, g)) != CPA_OK) return s;
-      if ((e = launch_block_scores_exact(tqq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) !=
-          cudaSuccess)
+    if ((s = make_map(&tp->tq, tp->w.qbar, 2, dims, str, box, "qbar")) != CPA_OK) return s;
+    if ((s = kv_map(&tp->tk, c->k_pages, g, c->num_pages, ps, hs, "k")) != CPA_OK) return s;
+    if (tp->exact && (s = q_map(&tp->tqq, q, g)) != CPA_OK) return s;
+  }
+  return CPA_OK;
+}
+
+int run_tables(const Geo& g, const TablesPlan& tp, cudaStream_t st) {
+  cudaError_t e;
+  int* launches = &g_launches;
+  if (!tp.mask_in) {
+    if (tp.exact) {  // NEXT-1: SPEC's exact tile-max scorer (full QK^T)
+      if ((e = launch_block_scores_exact(tp.tqq, tp.tk, tp.page_table, g, tp.scores, tp.w.mstar_key, tp.num_sms, st,
+                                         launches)) != cudaSuccess)
         return cuda_fail(e, "block_scores_exact");
     } else {
-      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(q), g, w.qbar, w.mstar_key, w.done, st, launches)) !=
-          cudaSuccess)
+      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(tp.q), g, tp.w.qbar, tp.w.mstar_key, tp.w.done, st,
+                             launches)) != cudaSuccess)
         return cuda_fail(e, "pool_q");
-      if ((e = launch_block_scores(tq, tk, c->page_table, g, scores, w.mstar_key, num_sms, st, launches)) != cudaSuccess)
+      if ((e = launch_block_scores(tp.tq, tp.tk, tp.page_table, g, tp.scores, tp.w.mstar_key, tp.num_sms, st,
+                                   launches)) != cudaSuccess)
         return cuda_fail(e, "block_scores");
     }
-    if (p->flags & CPA_F_SCORES_OUT) {
-      if ((e = launch_row_max(w.mstar_key, g, out->row_max, st, launches)) != cudaSuccess)
+    if (tp.scores_out) {
+      if ((e = launch_row_max(tp.w.mstar_key, g, tp.t.row_max, st, launches)) != cudaSuccess)
         return cuda_fail(e, "row_max");
     }
   }
-  if (mask_in && out->dev_status) {
-    if ((e = cudaMemsetAsync(out->dev_status, 0, sizeof(int), st)) != cudaSuccess) return cuda_fail(e, "memset");
+  if (tp.mask_in && tp.t.dev_status) {
+    if ((e = cudaMemsetAsync(tp.t.dev_status, 0, sizeof(int), st)) != cudaSuccess) return cuda_fail(e, "memset");
   }
   // the pooled path's k_pool_q zeroes the tables counter; the other paths do it here
-  if (mask_in || (p->flags & CPA_F_EXACT_SCORES)) {
-    if ((e = cudaMemsetAsync(w.done, 0, sizeof(unsigned), st)) != cudaSuccess) return cuda_fail(e, "memset");
+  if (tp.mask_in || tp.exact) {
+    if ((e = cudaMemsetAsync(tp.w.done, 0, sizeof(unsigned), st)) != cudaSuccess) return cuda_fail(e, "memset");
   }
-  e = launch_tables(scores, w.mstar_key, g, mask_in ? out->mask_bits : nullptr,
-                    (!mask_in && (p->flags & CPA_F_MASK_OUT)) ? out->mask_bits : nullptr, w.gwords,
-                    mask_in ? out->dev_status : nullptr, w.done, out->kv_indptr, out->kv_indices, st, launches);
+  e = launch_tables(tp.scores, tp.w.mstar_key, g, tp.mask_in ? tp.t.mask_bits : nullptr,
+                    (!tp.mask_in && (g.flags & CPA_F_MASK_OUT)) ? tp.t.mask_bits : nullptr, tp.w.gwords,
+                    tp.mask_in ? tp.t.dev_status : nullptr, tp.w.done, tp.t.kv_indptr, tp.t.kv_indices, st, launches);
   if (e != cudaSuccess) return cuda_fail(e, "tables");
   return CPA_OK;
 }
@@ -343,16 +367,22 @@ struct OutSpec {
   long long stride, bstride;  // elements between tokens / batch entries
 };
 
-int attention_launch(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
-                     int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
-                     const int32_t* indices, void* o, cudaStream_t st, const uint32_t* mask = nullptr,
-                     const OutSpec* os = nullptr, void* ws = nullptr, size_t ws_bytes = 0) {
-  CUtensorMap tq, tk, tv;
-  int s;
-  if ((s = q_map(&tq, q, g)) != CPA_OK) return s;
-  if ((s = kv_map(&tk, k_pages, g, num_pages, ps, hs, "k")) != CPA_OK) return s;
-  if ((s = kv_map(&tv, v_pages, g, num_pages, ps, hs, "v")) != CPA_OK) return s;
+struct AttnPlan {
+  CUtensorMap tq, tk, tv, tkh;
   AttnArgs a;
+  int kind;  // 0: 1-CTA kernel, 1: 2-CTA per-unit grid, 2: 2-CTA persistent stream-K grid
+  SkSched sk;
+};
+
+int prep_attention(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
+                   int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
+                   const int32_t* indices, void* o, AttnPlan* ap, const uint32_t* mask = nullptr,
+                   const OutSpec* os = nullptr, void* ws = nullptr, size_t ws_bytes = 0) {
+  int s;
+  if ((s = q_map(&ap->tq, q, g)) != CPA_OK) return s;
+  if ((s = kv_map(&ap->tk, k_pages, g, num_pages, ps, hs, "k")) != CPA_OK) return s;
+  if ((s = kv_map(&ap->tv, v_pages, g, num_pages, ps, hs, "v")) != CPA_OK) return s;
+  AttnArgs& a = ap->a;
   a.page_table = page_table;
   a.indptr = indptr;
   a.indices = indices;
@@ -370,42 +400,59 @@ int attention_launch(const cpa_params* p, const Geo& g, const void* q, const voi
     a.o_stride = g.q_stride;
     a.o_bstride = g.b_stride;
   }
-  cudaError_t e;
+  ap->kind = 0;
   if (attn_2cta_supported(g) && !(p->flags & CPA_F_NO_2CTA) && mask == nullptr) {
-    CUtensorMap tkh;  // half a page of keys per CTA of the pair
-    if ((s = kv_map(&tkh, k_pages, g, num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
+    // half a page of keys per CTA of the pair
+    if ((s = kv_map(&ap->tkh, k_pages, g, num_pages, ps, hs, "k_half", g.bs / 2)) != CPA_OK) return s;
     const int clusters = std::min(attn_2cta_max_clusters(g), kSkMaxClusters);
     // measured: on the sparse tables the per-unit grid is as fast (the chip is power-
     // bound, idle SM pairs are not lost time); on the dense baseline the persistent grid is 2-5% faster
     const bool auto_sk = indptr == nullptr && sk_wanted(g, clusters);
-    if (ws != nullptr && !(p->flags & CPA_F_NO_PERSIST) && (auto_sk || ((p->flags & CPA_F_PERSIST) && sk_wanted(g, clusters)))) {
+    ap->kind = 1;
+    if (ws != nullptr && !(p->flags & CPA_F_NO_PERSIST) &&
+        (auto_sk || ((p->flags & CPA_F_PERSIST) && sk_wanted(g, clusters)))) {
       if (ws_bytes < attn_ws_bytes(g)) return fail(CPA_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, attn_ws_bytes(g));
-      SkSched sk = carve_sk(g, ws, clusters);
-      e = launch_paged_attention_2cta(tq, tkh, tv, g, a, &sk, st, &g_launches);
-    } else {
-      e = launch_paged_attention_2cta(tq, tkh, tv, g, a, nullptr, st, &g_launches);
+      ap->sk = carve_sk(g, ws, clusters);
+      ap->kind = 2;
     }
-  } else {
-    e = launch_paged_attention(tq, tk, tv, g, a, st, &g_launches);
   }
+  return CPA_OK;
+}
+
+int run_attention(const Geo& g, const AttnPlan& ap, cudaStream_t st) {
+  cudaError_t e;
+  if (ap.kind == 0) e = launch_paged_attention(ap.tq, ap.tk, ap.tv, g, ap.a, st, &g_launches);
+  else e = launch_paged_attention_2cta(ap.tq, ap.tkh, ap.tv, g, ap.a, ap.kind == 2 ? &ap.sk : nullptr, st, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "paged_attention");
   return CPA_OK;
 }
 
-int attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
-                   long long hs, const cpa_tables* t, void* o, cudaStream_t st, const OutSpec* os, void* ws,
-                   size_t ws_bytes) {
+int attention_launch(const cpa_params* p, const Geo& g, const void* q, const void* k_pages, const void* v_pages,
+                     int num_pages, long long ps, long long hs, const int32_t* page_table, const int32_t* indptr,
+                     const int32_t* indices, void* o, cudaStream_t st, const uint32_t* mask = nullptr) {
+  AttnPlan ap;
+  int s;
+  if ((s = prep_attention(p, g, q, k_pages, v_pages, num_pages, ps, hs, page_table, indptr, indices, o, &ap, mask)) !=
+      CPA_OK)
+    return s;
+  return run_attention(g, ap, st);
+}
+
+int prep_attention_impl(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_cache* c, long long ps,
+                        long long hs, const cpa_tables* t, void* o, const OutSpec* os, void* ws, size_t ws_bytes,
+                        AttnPlan* ap) {
   if (!q || (!o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
   if (!aligned16(q) || (!os && !aligned16(o))) return fail(CPA_ERR_MISALIGNED, "q/o not 16B aligned");
   if (t && (!t->kv_indptr || !t->kv_indices)) return fail(CPA_ERR_NULL, "tables pointers");
   if (attn_2cta_supported(g) && !(p->flags & (CPA_F_NO_2CTA | CPA_F_NO_PERSIST)) && attn_ws_bytes(g) > 0 &&
       ws_bytes < attn_ws_bytes(g))
     return fail(CPA_ERR_WORKSPACE, "paged attention needs cpa_workspace_bytes() of workspace");
-  return attention_launch(p, g, q, c->k_pages, c->v_pages, c->num_pages, ps, hs, c->page_table,
-                          t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, st, nullptr, os, ws, ws_bytes);
+  return prep_attention(p, g, q, c->k_pages, c->v_pages, c->num_pages, ps, hs, c->page_table,
+                        t ? t->kv_indptr : nullptr, t ? t->kv_indices : nullptr, o, ap, nullptr, os, ws, ws_bytes);
 }
 
-// append (optional) -> estimator + tables -> attention, the body of cpa_chunk_step(_peer)
+// append (optional) -> estimator + tables -> attention, the body of cpa_chunk_step(_peer). Everything
+// is validated and planned before the append's launch (cpa.h: a failing call leaves outputs untouched).
 int chunk_step_impl(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
                     const cpa_kv_cache* cache, cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
                     cudaStream_t st, const OutSpec* os) {
@@ -418,20 +465,18 @@ int chunk_step_impl(const cpa_params* p, const void* q, const void* k_chunk, con
   if ((k_chunk == nullptr) != (v_chunk == nullptr)) return fail(CPA_ERR_NULL, "k_chunk/v_chunk: both or neither");
   if (!q || (!o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
   if (!tables) return fail(CPA_ERR_NULL, "tables is NULL");
-  int total = 0;
+  if (k_chunk && (!aligned16(k_chunk) || !aligned16(v_chunk)))
+    return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
+  TablesPlan tp;
+  AttnPlan ap;
+  if ((s = prep_tables(p, g, q, cache, ps, hs, tables, ws, ws_bytes, sms, &tp)) != CPA_OK) return s;
+  if ((s = prep_attention_impl(p, g, q, cache, ps, hs, tables, o, os, ws, ws_bytes, &ap)) != CPA_OK) return s;
   if (k_chunk) {
-    if (!aligned16(k_chunk) || !aligned16(v_chunk)) return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
-    cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, st, &g_launches);
+    cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, sms, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "append");
   }
-  total += g_launches;
-  g_launches = 0;
-  if ((s = build_tables_impl(p, g, q, cache, ps, hs, tables, ws, ws_bytes, st, sms)) != CPA_OK) return s;
-  total += g_launches;
-  g_launches = 0;
-  if ((s = attention_impl(p, g, q, cache, ps, hs, tables, o, st, os, ws, ws_bytes)) != CPA_OK) return s;
-  g_launches += total;
-  return CPA_OK;
+  if ((s = run_tables(g, tp, st)) != CPA_OK) return s;
+  return run_attention(g, ap, st);
 }
 
 int check_peers(const cpa_peer_out* pr) {
@@ -483,7 +528,9 @@ int cpa_build_tables(const cpa_params* p, const void* q, const cpa_kv_cache* cac
   if ((s = make_geo(p, &g)) != CPA_OK) return s;
   if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
   if ((s = device_info(&sms)) != CPA_OK) return s;
-  return build_tables_impl(p, g, q, cache, ps, hs, out, ws, ws_bytes, (cudaStream_t)stream, sms);
+  TablesPlan tp;
+  if ((s = prep_tables(p, g, q, cache, ps, hs, out, ws, ws_bytes, sms, &tp)) != CPA_OK) return s;
+  return run_tables(g, tp, (cudaStream_t)stream);
 }
 
 int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* cache, const cpa_tables* tables,
@@ -495,7 +542,9 @@ int cpa_paged_attention(const cpa_params* p, const void* q, const cpa_kv_cache* 
   if ((s = make_geo(p, &g)) != CPA_OK) return s;
   if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
   if ((s = device_info(&sms)) != CPA_OK) return s;
-  return attention_impl(p, g, q, cache, ps, hs, tables, o, (cudaStream_t)stream, nullptr, ws, ws_bytes);
+  AttnPlan ap;
+  if ((s = prep_attention_impl(p, g, q, cache, ps, hs, tables, o, nullptr, ws, ws_bytes, &ap)) != CPA_OK) return s;
+  return run_attention(g, ap, (cudaStream_t)stream);
 }
 
 int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk, const cpa_kv_cache* cache,
@@ -509,7 +558,7 @@ int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk,
   if ((s = device_info(&sms)) != CPA_OK) return s;
   if (!k_chunk || !v_chunk) return fail(CPA_ERR_NULL, "k_chunk/v_chunk NULL");
   if (!aligned16(k_chunk) || !aligned16(v_chunk)) return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
-  cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, (cudaStream_t)stream, &g_launches);
+  cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, sms, (cudaStream_t)stream, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "append");
   return CPA_OK;
 }
@@ -521,37 +570,66 @@ int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chunk, cons
   return chunk_step_impl(p, q, k_chunk, v_chunk, cache, tables, o, ws, ws_bytes, (cudaStream_t)stream, nullptr);
 }
 
+}  // extern "C"
+
+namespace {
+// OutSpec of a peer exchange: this rank's head slice of every rank's gathered buffer, own buffer first,
+// then the peers in rotated order (spreads the NVLink load).
+int peer_outspec(const cpa_params* p, const Geo& g, const cpa_peer_out* peers, OutSpec* os) {
+  int s;
+  if ((s = check_peers(peers)) != CPA_OK) return s;
+  if (!peers->peer_out) return fail(CPA_ERR_NULL, "peer_out is NULL");
+  const int W = peers->world;
+  const long long row = (long long)W * g.Hq * g.d;
+  os->n = W;
+  os->stride = peers->out_token_stride ? peers->out_token_stride : row;
+  if (os->stride < row || os->stride % 8)
+    return fail(CPA_ERR_SHAPE, "out_token_stride must be >= W*Hq*d, multiple of 8");
+  os->bstride = (long long)g.C * os->stride;
+  const size_t esz = (p->flags & CPA_F_OUT_F32) ? 4 : 2;
+  for (int k = 0; k < W; ++k) {
+    const int w = (peers->rank + k) % W;
+    if (!peers->peer_out[w]) return fail(CPA_ERR_NULL, "peer_out[%d] is NULL", w);
+    if (!aligned16(peers->peer_out[w])) return fail(CPA_ERR_MISALIGNED, "peer_out[%d] not 16B aligned", w);
+    os->outs[k] = reinterpret_cast<uint8_t*>(peers->peer_out[w]) + (size_t)peers->rank * g.Hq * g.d * esz;
+  }
+  return CPA_OK;
+}
+}  // namespace
+
+extern "C" {
+
 int cpa_chunk_step_peer(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
                         const cpa_kv_cache* cache, cpa_tables* tables, const cpa_peer_out* peers, void* ws,
                         size_t ws_bytes, void* stream) {
   g_launches = 0;
   Geo g;
   int s;
-  if ((s = make_geo(p, &g)) != CPA_OK) return s;
-  if ((s = check_peers(peers)) != CPA_OK) return s;
-  if (!peers->peer_out) return fail(CPA_ERR_NULL, "peer_out is NULL");
-  const int W = peers->world;
-  const long long row = (long long)W * g.Hq * g.d;
   OutSpec os;
-  os.n = W;
-  os.stride = peers->out_token_stride ? peers->out_token_stride : row;
-  if (os.stride < row || os.stride % 8) return fail(CPA_ERR_SHAPE, "out_token_stride must be >= W*Hq*d, multiple of 8");
-  os.bstride = (long long)g.C * os.stride;
-  const size_t esz = (p->flags & CPA_F_OUT_F32) ? 4 : 2;
-  for (int k = 0; k < W; ++k) {  // own buffer first, then the peers in rotated order (spreads NVLink load)
-    const int w = (peers->rank + k) % W;
-    if (!peers->peer_out[w]) return fail(CPA_ERR_NULL, "peer_out[%d] is NULL", w);
-    if (!aligned16(peers->peer_out[w])) return fail(CPA_ERR_MISALIGNED, "peer_out[%d] not 16B aligned", w);
-    os.outs[k] = reinterpret_cast<uint8_t*>(peers->peer_out[w]) + (size_t)peers->rank * g.Hq * g.d * esz;
-  }
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = peer_outspec(p, g, peers, &os)) != CPA_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   if ((s = chunk_step_impl(p, q, k_chunk, v_chunk, cache, tables, nullptr, ws, ws_bytes, st, &os)) != CPA_OK)
     return s;
-  const int n = g_launches;
+  return peer_barrier_impl(peers, st);
+}
+
+int cpa_paged_attention_peer(const cpa_params* p, const void* q, const cpa_kv_cache* cache, const cpa_tables* tables,
+                             const cpa_peer_out* peers, void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
-  if ((s = peer_barrier_impl(peers, st)) != CPA_OK) return s;
-  g_launches += n;
-  return CPA_OK;
+  Geo g;
+  int s, sms;
+  long long ps, hs;
+  OutSpec os;
+  if ((s = make_geo(p, &g)) != CPA_OK) return s;
+  if ((s = peer_outspec(p, g, peers, &os)) != CPA_OK) return s;
+  if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
+  if ((s = device_info(&sms)) != CPA_OK) return s;
+  AttnPlan ap;
+  if ((s = prep_attention_impl(p, g, q, cache, ps, hs, tables, nullptr, &os, ws, ws_bytes, &ap)) != CPA_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  if ((s = run_attention(g, ap, st)) != CPA_OK) return s;
+  return peer_barrier_impl(peers, st);
 }
 
 int cpa_peer_barrier(const cpa_peer_out* peers, void* stream) {

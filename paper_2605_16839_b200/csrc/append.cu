@@ -6,38 +6,66 @@
 
 namespace cpa {
 
-// flat grid-stride copy, one 16-byte vector per thread step: source [B, C, Hkv, d] is read
-// contiguously; each (token, head) row of d elements lands contiguous in its page slot.
+// One warp per chunk token (b, c): the token's page is looked up once, then the warp copies its
+// Hkv*d/8 16-byte vectors of K and of V (source [B, C, Hkv, d] contiguous, so every warp request is
+// 512 contiguous bytes; each (head, token) row of d elements lands contiguous in its page slot). All
+// loads of a token are issued before its stores (4 x 2 vectors per lane in flight for d=128, Hkv=8).
+// Grid: at most 8 resident 8-warp CTAs per SM, grid-stride over tokens.
+constexpr int kAppendUnroll = 4;
 __global__ void __launch_bounds__(256) k_append(const uint4* __restrict__ kc, const uint4* __restrict__ vc,
                                                 uint4* __restrict__ kp, uint4* __restrict__ vp,
                                                 const int32_t* __restrict__ pt, Geo g, long long ps, long long hs) {
-  const int per_tok = g.Hkv * (g.d / 8);
-  const long long total = (long long)g.B * g.C * per_tok;
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < total; x += (long long)gridDim.x * blockDim.x) {
-    const int e = (int)(x % (g.d / 8));
-    const long long r = x / (g.d / 8);
-    const int h = (int)(r % g.Hkv);
-    const long long bc = r / g.Hkv;
-    const int c = (int)(bc % g.C), b = (int)(bc / g.C);
-    const int t = g.P + c, j = t / g.bs, slot = t % g.bs;
+  const int lane = threadIdx.x & 31;
+  const int vshift = g.d == 128 ? 4 : 3;  // 16-byte vectors per (token, head) row: d/8
+  const int per_tok = g.Hkv << vshift;
+  const long long ntok = (long long)g.B * g.C;
+  const long long hs16 = hs >> 3, ps16 = ps >> 3;
+  const bool f16 = (g.flags & CPA_F_V_F16) != 0;
+  const long long wstride = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long tok = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tok < ntok; tok += wstride) {
+    const int b = (int)(tok / g.C);
+    const int t = g.P + (int)(tok - (long long)b * g.C);
+    const int j = t / g.bs;
     const int page = __ldg(pt + (long long)b * g.maxb + j);
-    const long long dst = ((long long)page * ps + (long long)h * hs + (long long)slot * g.d) / 8 + e;
-    kp[dst] = kc[x];
-    uint4 w = vc[x];
-    if (g.flags & CPA_F_V_F16) {  // V pool in fp16 (exact for bf16 values in fp16's normal range)
-      w.x = bf16x2_to_f16x2(w.x);
-      w.y = bf16x2_to_f16x2(w.y);
-      w.z = bf16x2_to_f16x2(w.z);
-      w.w = bf16x2_to_f16x2(w.w);
+    const long long dst0 = (long long)page * ps16 + (long long)(t - j * g.bs) * (g.d >> 3);
+    const uint4* ks = kc + tok * per_tok;
+    const uint4* vs = vc + tok * per_tok;
+    for (int x0 = 0; x0 < per_tok; x0 += 32 * kAppendUnroll) {
+      uint4 kr[kAppendUnroll], vr[kAppendUnroll];
+#pragma unroll
+      for (int u = 0; u < kAppendUnroll; ++u) {
+        const int x = x0 + u * 32 + lane;
+        if (x < per_tok) {
+          kr[u] = __ldcs(ks + x);  // read once: evict-first
+          vr[u] = __ldcs(vs + x);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kAppendUnroll; ++u) {
+        const int x = x0 + u * 32 + lane;
+        if (x < per_tok) {
+          const long long dst = dst0 + (long long)(x >> vshift) * hs16 + (x & ((1 << vshift) - 1));
+          kp[dst] = kr[u];
+          uint4 w = vr[u];
+          if (f16) {  // V pool in fp16 (exact for bf16 values in fp16's normal range, saturating beyond)
+            w.x = bf16x2_to_f16x2(w.x);
+            w.y = bf16x2_to_f16x2(w.y);
+            w.z = bf16x2_to_f16x2(w.z);
+            w.w = bf16x2_to_f16x2(w.w);
+          }
+          vp[dst] = w;
+        }
+      }
     }
-    vp[dst] = w;
   }
 }
 
 cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c, const Geo& g, long long ps,
-                          long long hs, cudaStream_t st, int* launches) {
-  const long long total = (long long)g.B * g.C * g.Hkv * (g.d / 8);
-  const int blocks = (int)((total + 255) / 256 < 148 * 8 ? (total + 255) / 256 : 148 * 8);
+                          long long hs, int num_sms, cudaStream_t st, int* launches) {
+  const long long ntok = (long long)g.B * g.C;
+  const long long need = (ntok + 7) / 8;         // 8 tokens (warps) per CTA
+  const long long cap = (long long)num_sms * 8;  // 8 resident 256-thread CTAs per SM
+  const int blocks = (int)(need < cap ? need : cap);
   k_append<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(kc), reinterpret_cast<const uint4*>(vc),
                                    reinterpret_cast<uint4*>(c.k_pages), reinterpret_cast<uint4*>(c.v_pages),
                                    c.page_table, g, ps, hs);

@@ -261,8 +261,15 @@ CPA_DEV uint32_t pack_f16x2(float lo, float hi) {
   __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// bf16x2 -> f16x2 for the fp16 V operand of P.V: round to nearest, SATURATING to +-65504 (a finite bf16
+// beyond fp16's range must not become inf: 0 * inf = NaN under a masked P); |v| < 2^-14 becomes an fp16
+// subnormal (cpa.h states the range).
 CPA_DEV uint32_t bf16x2_to_f16x2(uint32_t w) {
-  return pack_f16x2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+  uint32_t d;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;"
+      : "=r"(d)
+      : "f"(__uint_as_float(w & 0xffff0000u)), "f"(__uint_as_float(w << 16)));
+  return d;
 }
 CPA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 CPA_DEV float fast_exp2(float x) {

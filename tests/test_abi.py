@@ -97,3 +97,31 @@ def test_peer_validation(L, world, rank, kw, status):
     r = L.cpa_chunk_step_peer(ctypes.byref(p), 16, None, None, ctypes.byref(c), ctypes.byref(t), ctypes.byref(pr),
                               16, 1 << 30, None)
     assert r == status, L.cpa_last_error()
+
+
+@pytest.mark.parametrize("world,rank,kw,status", [
+    (0, 0, {}, 2), (2, 2, {}, 2), (2, 0, dict(sigs=None), 1), (2, 0, dict(outs=24), 4), (2, 0, dict(stride=100), 2),
+])
+def test_attention_peer_validation(L, world, rank, kw, status):
+    """cpa_paged_attention_peer validates the peer description before touching the device (cpa.h)."""
+    p = _p(num_q_heads=16, num_kv_heads=4)
+    pr, keep = _peer(world, rank, **kw)
+    c = cpa._Cache(16, 16, 0, 0, 16, 2048, 10)
+    r = L.cpa_paged_attention_peer(ctypes.byref(p), 16, ctypes.byref(c), None, ctypes.byref(pr), 16, 1 << 30, None)
+    assert r == status, L.cpa_last_error()
+
+
+def test_paged_kv_cache_num_pages():
+    """PagedKVCache: num_pages is shape[0] only for the default [pages, Hkv, bs, d] pool; explicit strides
+    (e.g. the per-sequence [B, Hkv, L, d] layout) need it given; the V dtype must match CPA_F_V_F16."""
+    import torch
+    kp = torch.zeros(4, 2, 16, 64, dtype=torch.bfloat16)
+    pt = torch.zeros(1, 4, dtype=torch.int32)
+    assert cpa.PagedKVCache(kp, kp, pt)._c().num_pages == 4
+    with pytest.raises(ValueError):
+        cpa.PagedKVCache(kp, kp, pt, page_stride=16 * 64, head_stride=64 * 64)._c()
+    assert cpa.PagedKVCache(kp, kp, pt, page_stride=16 * 64, head_stride=64 * 64, num_pages=4)._c().num_pages == 4
+    p = cpa.make_params(1, 4, 2, 64, 16, 16, 48, flags=cpa.F_V_F16)
+    with pytest.raises(ValueError):
+        cpa.PagedKVCache(kp, kp, pt)._check_v(p)
+    cpa.PagedKVCache(kp, kp.half(), pt)._check_v(p)

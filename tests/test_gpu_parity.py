@@ -495,3 +495,43 @@ def test_v_f16_pool_other_paths_bitwise():
             res[flag] = outs
         for a, b in zip(res[0], res[cpa.F_V_F16]):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("pool", ["f16", "bf16"])
+def test_v_beyond_fp16_range_saturates(pool):
+    """P.V runs in fp16 (K3), so V is converted to fp16 -- once at append (CPA_F_V_F16) or per
+    page in the kernel (bf16 pool). cpa.h: the conversion rounds to nearest and SATURATES to +-65504,
+    so a finite bf16 V beyond fp16's range never becomes inf (masked P = 0 times inf would be NaN).
+    The outputs must equal the oracle's with V clamped to [-65504, 65504]; values up to 65504 pass
+    through exactly (near-limit entries 65280 / 65504 / 61440 are fp16-representable)."""
+    Hq, Hkv, d, bs, C, P = 8, 2, 128, 128, 256, 512
+    q, k, v = random_qkv(1, Hq, Hkv, d, C, P + C, seed=77)
+    rng = np.random.default_rng(0)
+    big = np.array([65280.0, 65504.0, 61440.0, -65504.0, 65536.0, -98304.0, 1.0e5, 3.0e38], np.float32)
+    idx = rng.integers(0, v.size, size=4096)
+    v.reshape(-1)[idx] = big[rng.integers(0, len(big), size=idx.size)]
+    from synth.workload import round_bf16
+    v = round_bf16(v)  # 1e5 / 3e38 -> nearest bf16 (still finite, beyond fp16)
+    assert np.isfinite(v).all() and np.abs(v).max() > 65504
+    flag = cpa.F_V_F16 if pool == "f16" else 0
+    case = Case(q, k, v, P, bs, seed=5, flags=cpa.F_OUT_F32 | flag)
+    kc = to_dev_bf16(np.ascontiguousarray(k[:, :, P:].transpose(0, 2, 1, 3)))
+    vc = to_dev_bf16(np.ascontiguousarray(v[:, :, P:].transpose(0, 2, 1, 3)))
+    if pool == "f16":  # prefix pages converted by the device append of the whole sequence, chunk by chunk
+        vp = torch.zeros_like(case.cache.v_pages, dtype=torch.float16)
+        case.cache = cpa.PagedKVCache(case.cache.k_pages, vp, case.cache.page_table)
+        for c0 in range(0, P + C, C):
+            pa = cpa.make_params(1, Hq, Hkv, d, bs, C, c0, flags=flag)
+            cpa.append_kv(pa, to_dev_bf16(np.ascontiguousarray(k[:, :, c0:c0 + C].transpose(0, 2, 1, 3))),
+                          to_dev_bf16(np.ascontiguousarray(v[:, :, c0:c0 + C].transpose(0, 2, 1, 3))), case.cache)
+        torch.cuda.synchronize()
+        assert float(vp.abs().max()) == 65504.0 and bool(torch.isfinite(vp).all())
+    t = cpa.alloc_tables(case.params)
+    o = case.out(True)
+    cpa.chunk_step(case.params, case.dq, case.cache, t, o, kc, vc)
+    torch.cuda.synchronize()
+    got = o.cpu().numpy().astype(np.float64)
+    assert np.isfinite(got).all()
+    ip, ix = tables_to_numpy(t)
+    ref = O.paged_attention(q, k, np.clip(v, -65504.0, 65504.0), P, bs, ip, ix)
+    assert rel_err(got, ref) <= ATOL_REL

@@ -55,7 +55,7 @@ def main():
     for s in range(args.parts):
         ps = cpa.make_params(B, h * E, h, d, bs, C, P, alpha=0.06, flags=cpa.F_V_F16, q_token_stride=Hq * d)
         cs = cpa.PagedKVCache(kp[:, s * h:(s + 1) * h], vp[:, s * h:(s + 1) * h], ptab,
-                              page_stride=Hkv * bs * d, head_stride=bs * d)
+                              page_stride=Hkv * bs * d, head_stride=bs * d, num_pages=kp.shape[0])
         parts.append(dict(p=ps, cache=cs, t=cpa.alloc_tables(ps),
                           ws=torch.empty(cpa.workspace_bytes(ps), dtype=torch.uint8, device="cuda"),
                           q=dq[:, :, s * h * E:(s + 1) * h * E], o=o2[:, :, s * h * E:(s + 1) * h * E],
