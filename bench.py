@@ -82,12 +82,13 @@ def bench_config(args, world):
     graph = not args.no_graph and not one_dev and (world == 1 or args.collective == "peer")
     return {"workload": cfg.name, "batch": cfg.batch, "context": cfg.context, "chunk": cfg.chunk,
             "prefix": P, "q_heads": cfg.num_q_heads, "kv_heads": cfg.num_kv_heads, "head_dim": cfg.head_dim,
-            "block_size": cfg.block_size, "alpha": ALPHA, "needle_density": RHO,
+            "block_size": cfg.block_size, "alpha": ALPHA, "needle_density": args.rho,
             "exec_group_size": args.exec_group or cfg.group_size,
             "scorer": "exact tile max (SPEC.md:223)" if args.exact_scores else "pooled query (SPEC.md:269)",
             "parallelism": par, "l2": "flushed (512 MiB write) before every timed step",
             "launch": "CUDA graph of the chunk step" if graph else "direct",
-            "v_cache_dtype": "f16" if args.v_f16 else "bf16"}
+            "v_cache_dtype": "f16" if args.v_f16 else "bf16",
+            **({"workload_variant": args.variant} if args.variant != "base" else {})}
 
 
 # ------------------------------------------------------------------------------ algorithmic work
@@ -228,8 +229,8 @@ def oracle_chunk(args, rows_per_group=None, log=None):
     E = args.exec_group or E_kv
     Gn = cfg.num_q_heads // E
     t_gen = time.perf_counter()
-    k, v = make_kv(cfg, seed, RHO)
-    q = make_q(cfg, seed)
+    k, v = make_kv(cfg, seed, args.rho, variant=args.variant)
+    q = make_q(cfg, seed, variant=args.variant)
     _OR.update(q=q, k=k, v=v, P=P, C=C, bs=cfg.block_size, E=E, E_kv=E_kv, Gn=Gn, exact=args.exact_scores)
     cores = host_cores()
     groups = cfg.batch * Gn
@@ -309,6 +310,7 @@ def cpu_baseline_leg(args):
         cmd.append("--v-bf16")
     if args.no_graph:
         cmd.append("--no-graph")
+    cmd += ["--rho", str(args.rho), "--variant", args.variant]
     env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
@@ -383,8 +385,8 @@ def run_gpu(args):
     from paper_2605_16839_b200.shard import allgather_heads, head_shard
     kvh, qh = head_shard(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
     hkv_l, hq_l = len(kvh), len(qh)
-    k, v = make_kv(cfg, seed, RHO, kv_heads=kvh)
-    q = make_q(cfg, seed, q_heads=qh)
+    k, v = make_kv(cfg, seed, args.rho, kv_heads=kvh, variant=args.variant)
+    q = make_q(cfg, seed, q_heads=qh, variant=args.variant)
     nkvb = -(-L // bs)
     pt, npages = page_layout(cfg.batch, nkvb, seed)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
@@ -605,7 +607,7 @@ def run_gpu(args):
     except Exception:
         pass
 
-    cpu = cpu_baseline_leg(args) if rank == 0 else None
+    cpu = cpu_baseline_leg(args) if rank == 0 and not args.no_cpu else None
     if rank == 0:
         out = {
             "metric": METRIC, "value": round(ms, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -679,6 +681,10 @@ def main():
                          "default fp16 pool (CPA_F_V_F16: converted once at append; bitwise-identical outputs)")
     ap.add_argument("--collective", default="peer", choices=["peer", "nccl"],
                     help="N>1 head-output all-gather: fused P2P stores in the attention epilogue, or NCCL")
+    ap.add_argument("--rho", type=float, default=RHO, help="needle density of the planted workload (NEXT-4 sweep)")
+    ap.add_argument("--variant", default="base", choices=["base", "qdiverse"],
+                    help="workload variant (synth/workload.py; qdiverse: union density grows with chunk size)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -21,6 +21,12 @@ planted high-score 'needle' blocks").
     its queries get +beta_q * sum u_c (for GQA 8 the two 4-head sub-groups cover
     overlapping but different topic sets, so sub-KV-group union keeps fewer blocks);
   * beta_q * beta_k / sqrt(d) = 6 (needle pooled logit ~ 6 vs background ~0.3).
+Variant "qdiverse" (NEXT-4 chunk-size sweep): 64 topics per group, head
+pools of 32 topics offset by 16 per head, 2 topics per q-block. A q-block then sees few topics, so
+the Q-block union (and the group union) keeps more needles the more q-blocks a chunk has: the
+post-union density grows with the chunk size, the effect PAPER.md:644-645 names ("larger chunks
+increase Q-block union within each chunk, reducing effective sparsity"). Expected coverage of the
+group's topics after the union of nqb q-blocks: 1 - (15/16)^(2 nqb).
 Random numbers come from numpy Philox keyed by (seed, tensor, b, head, chunk), so
 any slice (one KV head for one rank, one chunk's Q) regenerates identically.
 """
@@ -93,8 +99,23 @@ def round_bf16(x: np.ndarray) -> np.ndarray:
     return (u.astype(np.uint32)).view(np.float32)
 
 
-def n_topics(cfg: "Config") -> int:
+# per variant: topics per group, topics per head pool, pool offset between heads, topics per q-block
+VARIANTS = {"base": None, "qdiverse": (64, 32, 16, 2)}
+
+
+def n_topics(cfg: "Config", variant: str = "base") -> int:
+    if variant != "base":
+        return VARIANTS[variant][0]
     return 3 * cfg.group_size if cfg.group_size > 4 else N_TOPICS
+
+
+def _pool(cfg: "Config", hl: int, variant: str):
+    """Topic pool of query head hl (local index in its group) and the number drawn per q-block."""
+    if variant != "base":
+        nt, size, stride, per = VARIANTS[variant]
+        return [(stride * hl + s) % nt for s in range(size)], per
+    nt = n_topics(cfg)
+    return [(3 * hl + s) % nt for s in range(TOPICS_PER_POOL)], TOPICS_PER_QBLOCK
 
 
 def _topics(seed: int, b: int, g: int, d: int, nt: int = N_TOPICS) -> np.ndarray:
@@ -104,7 +125,7 @@ def _topics(seed: int, b: int, g: int, d: int, nt: int = N_TOPICS) -> np.ndarray
     return qmat.astype(np.float32)  # d x nt, orthonormal columns
 
 
-def needle_plan(cfg: Config, seed: int, rho: float, b: int, g: int):
+def needle_plan(cfg: Config, seed: int, rho: float, b: int, g: int, variant: str = "base"):
     """Needle blocks (ascending) and their topics for group (b, g)."""
     bs = cfg.block_size
     pb_max = (cfg.context - cfg.chunk) // bs if cfg.context > cfg.chunk else 0
@@ -112,7 +133,11 @@ def needle_plan(cfg: Config, seed: int, rho: float, b: int, g: int):
     n_n = int(round(rho * n_cand))
     rng = _key(seed, "plan", b, g)
     blocks = np.sort(rng.choice(np.arange(1, pb_max), size=n_n, replace=False)) if n_n > 0 else np.zeros(0, np.int64)
-    topics = rng.integers(0, n_topics(cfg), size=n_n)
+    if variant == "base":
+        topics = rng.integers(0, n_topics(cfg, variant), size=n_n)
+    else:  # balanced: every topic owns floor or ceil(n_n / T) needles (no q-block without a needle)
+        nt = n_topics(cfg, variant)
+        topics = rng.permutation(np.arange(n_n) % nt) if n_n > 0 else np.zeros(0, np.int64)
     return blocks, topics
 
 
@@ -122,7 +147,8 @@ def _betas(d: int):
 
 
 def make_kv(cfg: Config, seed: int, rho: float = 0.30, length: Optional[int] = None,
-            kv_heads: Optional[range] = None, needles: bool = True, graded: bool = False):
+            kv_heads: Optional[range] = None, needles: bool = True, graded: bool = False,
+            variant: str = "base"):
     """Logical flat K, V [B, Hkv_sel, L, d] float32 (bf16-valued).
 
     graded=True (alpha-sweep workload): needle j's key boost is scaled by
@@ -140,9 +166,9 @@ def make_kv(cfg: Config, seed: int, rho: float = 0.30, length: Optional[int] = N
             kk = rng.standard_normal((L, d), dtype=np.float32)
             vv = rng.standard_normal((L, d), dtype=np.float32)
             if needles:
-                U = _topics(seed, b, g, d, n_topics(cfg))
+                U = _topics(seed, b, g, d, n_topics(cfg, variant))
                 kk -= (kk @ U) @ U.T
-                blocks, topics = needle_plan(cfg, seed, rho, b, g)
+                blocks, topics = needle_plan(cfg, seed, rho, b, g, variant)
                 gains = (_key(seed, "grade", b, g).uniform(0.1, 1.0, size=len(blocks)) if graded
                          else np.ones(len(blocks)))
                 bs = cfg.block_size
@@ -156,7 +182,7 @@ def make_kv(cfg: Config, seed: int, rho: float = 0.30, length: Optional[int] = N
 
 
 def make_q(cfg: Config, seed: int, chunk_index: Optional[int] = None,
-           q_heads: Optional[range] = None, needles: bool = True):
+           q_heads: Optional[range] = None, needles: bool = True, variant: str = "base"):
     """Q of one chunk, [B, C, Hq_sel, d] float32 (bf16-valued)."""
     P, C, _ = cfg.chunk_geometry(chunk_index)
     t = P // cfg.chunk
@@ -170,13 +196,12 @@ def make_q(cfg: Config, seed: int, chunk_index: Optional[int] = None,
             qq = rng.standard_normal((C, d), dtype=np.float32)
             if needles:
                 g, hl = h // E, h % E
-                nt = n_topics(cfg)
-                U = _topics(seed, b, g, d, nt)
+                U = _topics(seed, b, g, d, n_topics(cfg, variant))
                 qq -= (qq @ U) @ U.T
-                pool = [(3 * hl + s) % nt for s in range(TOPICS_PER_POOL)]
+                pool, per = _pool(cfg, hl, variant)
                 nqb = -(-C // bs)
                 for i in range(nqb):
-                    sel = rng.choice(pool, size=TOPICS_PER_QBLOCK, replace=False)
+                    sel = rng.choice(pool, size=per, replace=False)
                     boost = beta_q * U[:, sel].sum(axis=1)
                     qq[i * bs:min((i + 1) * bs, C)] += boost
             q[b, :, hi] = round_bf16(qq)

@@ -36,7 +36,7 @@ def test_reference_arm_config_matches_gpu_arm_flags():
     import argparse
     import bench
     a = argparse.Namespace(config="llama8b_128k", exec_group=0, exact_scores=False, collective="peer",
-                           no_graph=False, v_f16=True)
+                           no_graph=False, v_f16=True, rho=0.3, variant="base")
     c1 = bench.bench_config(a, 1)
     assert c1["workload"] == "llama8b_128k" and c1["launch"].startswith("CUDA graph") and c1["v_cache_dtype"] == "f16"
     assert bench.bench_config(a, 8)["parallelism"].startswith("kv-group shard x8 + fused peer-store")

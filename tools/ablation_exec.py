@@ -15,9 +15,9 @@ import paper_2605_16839_b200 as cpa
 from synth.workload import CONFIGS, make_kv, make_q, page_layout, to_pool
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--context", type=int, default=65536)
+ap.add_argument("--context", type=int, default=131072)
 ap.add_argument("--chunk", type=int, default=512)
-ap.add_argument("--batches", default="1,2,4,8")
+ap.add_argument("--batches", default="1,2,4,8,16")
 args = ap.parse_args()
 ev = lambda: torch.cuda.Event(enable_timing=True)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
@@ -28,13 +28,13 @@ for B in [int(x) for x in args.batches.split(",")]:
     k, v = make_kv(cfg, seed); q = make_q(cfg, seed)
     pt, npg = page_layout(B, -(-L // bs), seed)
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16)
-    cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)), torch.from_numpy(pt).cuda())
+    cache = cpa.PagedKVCache(dev(to_pool(k, pt, npg, bs)), dev(to_pool(v, pt, npg, bs)).half(), torch.from_numpy(pt).cuda())  # fp16 V pool (bench default)
     dq = dev(q); del k, v
-    p = cpa.make_params(B, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06)
+    p = cpa.make_params(B, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06, flags=cpa.F_V_F16)
     t = cpa.alloc_tables(p, mask=True)
     nqb, nkvb, pb, Gn, nwords, Rpad = cpa.geometry(p)
     qmask = torch.empty(B, cfg.num_q_heads, nqb, nwords, dtype=torch.int32, device="cuda")
-    pm = cpa.make_params(B, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06, flags=cpa.F_MASK_OUT)
+    pm = cpa.make_params(B, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, bs, C, P, alpha=0.06, flags=cpa.F_MASK_OUT | cpa.F_V_F16)
     ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
     cws = torch.empty(int(cpa.lib().cpa_copy_workspace_bytes(__import__("ctypes").byref(p))), dtype=torch.uint8, device="cuda")
     o = torch.empty(B, C, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
