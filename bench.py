@@ -447,9 +447,9 @@ def run_gpu(args):
         g = torch.cuda.CUDAGraph()
         # thread_local: the NCCL watchdog thread may query events while this thread captures
         with torch.cuda.graph(g, capture_error_mode="thread_local"):
-            # == cpa_chunk_step(_peer): append + build_tables + attention (same workspace, same stream)
-            cpa.append_kv(p_, kc, vc, cache_)
-            cpa.build_tables(p_, dq, cache_, tables, workspace=ws)
+            # == cpa_chunk_step(_peer): prepare (append + estimator + tables) + attention (same workspace,
+            # same stream), split so that event nodes bracket the attention kernel
+            cpa.prepare_chunk(p_, dq, cache_, tables, kc, vc, workspace=ws)
             ev[0].record()
             if peers is not None:
                 cpa.paged_attention_peer(p_, dq, cache_, tables, peers, workspace=ws)

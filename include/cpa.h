@@ -80,10 +80,13 @@ enum {
   CPA_F_NO_2CTA = 512u,   /* ablation: single-CTA attention kernel instead of the cta_group::2 pair */
   CPA_F_NO_PERSIST = 1024u, /* ablation: one cluster per work unit instead of the persistent stream-K grid */
   CPA_F_PERSIST = 2048u,  /* ablation / tests: persistent stream-K grid whenever B*Gn <= 4 */
-  CPA_F_V_F16 = 4096u     /* the V pool holds fp16 (cpa_append_kv converts the bf16 chunk; exact for bf16
+  CPA_F_V_F16 = 4096u,    /* the V pool holds fp16 (cpa_append_kv converts the bf16 chunk; exact for bf16
                              values in fp16's normal range, i.e. the conversion the attention kernels
-                             otherwise do per page): the attention kernels skip their V conversion.
-                             Incompatible with CPA_F_P_BF16. */
+                             otherwise do per page; |v| > 65504 saturates to +-65504, |v| < 2^-14 becomes
+                             an fp16 subnormal): the attention kernels skip their V conversion.
+                             Incompatible with CPA_F_P_BF16. The bf16-pool path converts V per page with
+                             the same saturating rounding (P.V runs in fp16 either way, K3). */
+  CPA_F_NO_PDL = 8192u    /* ablation: launch the step's kernels without programmatic dependent launch */
 };
 
 typedef struct {
@@ -179,6 +182,14 @@ CPA_API int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chu
  * token slots [P, P+C) of each sequence's pages. K/V pools are written in place. */
 CPA_API int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk,
                   const cpa_kv_cache* cache, void* stream);
+
+/* The first half of cpa_chunk_step: optional append of the chunk's K/V, then the estimator and the
+ * tables (rows a0-a5), i.e. cpa_append_kv + cpa_build_tables as one call, so the append and the query
+ * pooling may overlap (programmatic dependent launch). cpa_chunk_step == cpa_prepare_chunk followed by
+ * cpa_paged_attention over the tables. Arguments and errors as cpa_chunk_step (no o). */
+CPA_API int cpa_prepare_chunk(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                              const cpa_kv_cache* cache, cpa_tables* tables, void* ws, size_t ws_bytes,
+                              void* stream);
 
 /* ---- Multi-GPU: head-group sharding with the output all-gather fused into the attention epilogue.
  * The chunk step shards by execution group with no data-path exchange: every table is per (b, g)

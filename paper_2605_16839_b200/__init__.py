@@ -16,7 +16,7 @@ import torch
 
 __all__ = [
     "CpaError", "Params", "PagedKVCache", "BlockTables", "lib", "make_params", "workspace_bytes",
-    "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "last_launch_count",
+    "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "prepare_chunk", "last_launch_count",
     "paged_attention_copy", "block_sparse_attention", "expand_tables", "PeerOut", "chunk_step_peer",
     "paged_attention_peer", "peer_barrier", "HostChunkStream",
     "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "F_NO_PERSIST", "F_PERSIST", "F_V_F16", "EXPORTED_SYMBOLS",
@@ -30,7 +30,7 @@ F_NO_PERSIST, F_PERSIST, F_V_F16 = 1024, 2048, 4096
 STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA_ERR_MISALIGNED",
           "CPA_ERR_ALPHA", "CPA_ERR_WORKSPACE", "CPA_ERR_CAPACITY", "CPA_ERR_CUDA"]
 EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",
-                    "cpa_append_kv", "cpa_copy_workspace_bytes", "cpa_paged_attention_copy",
+                    "cpa_append_kv", "cpa_prepare_chunk", "cpa_copy_workspace_bytes", "cpa_paged_attention_copy",
                     "cpa_block_sparse_attention", "cpa_expand_tables", "cpa_chunk_step_peer",
                     "cpa_paged_attention_peer", "cpa_peer_barrier", "cpa_status_string", "cpa_last_error", "cpa_version", "cpa_last_launch_count"]
 
@@ -87,6 +87,8 @@ def lib() -> ctypes.CDLL:
         L.cpa_chunk_step.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(_Cache),
                                      ctypes.POINTER(_Tables), vp, vp, ctypes.c_size_t, vp]
         L.cpa_append_kv.argtypes = [ctypes.POINTER(Params), vp, vp, ctypes.POINTER(_Cache), vp]
+        L.cpa_prepare_chunk.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(_Cache),
+                                        ctypes.POINTER(_Tables), vp, ctypes.c_size_t, vp]
         L.cpa_copy_workspace_bytes.argtypes = [ctypes.POINTER(Params)]
         L.cpa_copy_workspace_bytes.restype = ctypes.c_size_t
         L.cpa_paged_attention_copy.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache),
@@ -103,7 +105,7 @@ def lib() -> ctypes.CDLL:
         L.cpa_paged_attention_peer.argtypes = [ctypes.POINTER(Params), vp, ctypes.POINTER(_Cache),
                                                ctypes.POINTER(_Tables), ctypes.POINTER(_PeerOut), vp,
                                                ctypes.c_size_t, vp]
-        for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv,
+        for f in (L.cpa_build_tables, L.cpa_paged_attention, L.cpa_chunk_step, L.cpa_append_kv, L.cpa_prepare_chunk,
                   L.cpa_chunk_step_peer, L.cpa_peer_barrier, L.cpa_paged_attention_peer):
             f.restype = i32
         L.cpa_status_string.argtypes = [i32]
@@ -251,6 +253,18 @@ def chunk_step(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTab
     _check(lib().cpa_chunk_step(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
                                 ctypes.byref(t), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
     return out
+
+
+def prepare_chunk(p: Params, q: torch.Tensor, cache: PagedKVCache, tables: BlockTables,
+                  k_chunk: Optional[torch.Tensor] = None, v_chunk: Optional[torch.Tensor] = None,
+                  workspace: Optional[torch.Tensor] = None, stream=None) -> BlockTables:
+    """cpa_prepare_chunk: append (optional) + estimator + tables, the first half of chunk_step."""
+    ws = _ws(p, workspace, q.device, stream)
+    cache._check_v(p)
+    c, t = cache._c(), tables._c()
+    _check(lib().cpa_prepare_chunk(ctypes.byref(p), _ptr(q), _ptr(k_chunk), _ptr(v_chunk), ctypes.byref(c),
+                                   ctypes.byref(t), _ptr(ws), ws.numel(), _stream(stream)))
+    return tables
 
 
 class PeerOut:

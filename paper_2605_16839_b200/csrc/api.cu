@@ -14,7 +14,7 @@
 
 namespace cpa {
 cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
-                          unsigned* tables_done, cudaStream_t st, int* launches);
+                          unsigned* tables_done, bool after_append, cudaStream_t st, int* launches);
 cudaError_t launch_block_scores(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,
                                 const Geo& g, float* scores, int* mstar_key, int num_sms,
                                 cudaStream_t st, int* launches);
@@ -324,7 +324,7 @@ int prep_tables(const cpa_params* p, const Geo& g, const void* q, const cpa_kv_c
   return CPA_OK;
 }
 
-int run_tables(const Geo& g, const TablesPlan& tp, cudaStream_t st) {
+int run_tables(const Geo& g, const TablesPlan& tp, cudaStream_t st, bool after_append = false) {
   cudaError_t e;
   int* launches = &g_launches;
   if (!tp.mask_in) {
@@ -333,7 +333,7 @@ int run_tables(const Geo& g, const TablesPlan& tp, cudaStream_t st) {
                                          launches)) != cudaSuccess)
         return cuda_fail(e, "block_scores_exact");
     } else {
-      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(tp.q), g, tp.w.qbar, tp.w.mstar_key, tp.w.done, st,
+      if ((e = launch_pool_q(reinterpret_cast<const __nv_bfloat16*>(tp.q), g, tp.w.qbar, tp.w.mstar_key, tp.w.done, after_append, st,
                              launches)) != cudaSuccess)
         return cuda_fail(e, "pool_q");
       if ((e = launch_block_scores(tp.tq, tp.tk, tp.page_table, g, tp.scores, tp.w.mstar_key, tp.num_sms, st,
@@ -455,7 +455,7 @@ int prep_attention_impl(const cpa_params* p, const Geo& g, const void* q, const 
 // is validated and planned before the append's launch (cpa.h: a failing call leaves outputs untouched).
 int chunk_step_impl(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
                     const cpa_kv_cache* cache, cpa_tables* tables, void* o, void* ws, size_t ws_bytes,
-                    cudaStream_t st, const OutSpec* os) {
+                    cudaStream_t st, const OutSpec* os, bool with_attention = true) {
   Geo g;
   int s, sms;
   long long ps, hs;
@@ -463,20 +463,21 @@ int chunk_step_impl(const cpa_params* p, const void* q, const void* k_chunk, con
   if ((s = check_cache(cache, &g, &ps, &hs)) != CPA_OK) return s;
   if ((s = device_info(&sms)) != CPA_OK) return s;
   if ((k_chunk == nullptr) != (v_chunk == nullptr)) return fail(CPA_ERR_NULL, "k_chunk/v_chunk: both or neither");
-  if (!q || (!o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
+  if (!q || (with_attention && !o && !os)) return fail(CPA_ERR_NULL, "q/o is NULL");
   if (!tables) return fail(CPA_ERR_NULL, "tables is NULL");
   if (k_chunk && (!aligned16(k_chunk) || !aligned16(v_chunk)))
     return fail(CPA_ERR_MISALIGNED, "k/v chunk not 16B aligned");
   TablesPlan tp;
   AttnPlan ap;
   if ((s = prep_tables(p, g, q, cache, ps, hs, tables, ws, ws_bytes, sms, &tp)) != CPA_OK) return s;
-  if ((s = prep_attention_impl(p, g, q, cache, ps, hs, tables, o, os, ws, ws_bytes, &ap)) != CPA_OK) return s;
+  if (with_attention && (s = prep_attention_impl(p, g, q, cache, ps, hs, tables, o, os, ws, ws_bytes, &ap)) != CPA_OK)
+    return s;
   if (k_chunk) {
     cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, sms, st, &g_launches);
     if (e != cudaSuccess) return cuda_fail(e, "append");
   }
-  if ((s = run_tables(g, tp, st)) != CPA_OK) return s;
-  return run_attention(g, ap, st);
+  if ((s = run_tables(g, tp, st, k_chunk != nullptr)) != CPA_OK) return s;
+  return with_attention ? run_attention(g, ap, st) : CPA_OK;
 }
 
 int check_peers(const cpa_peer_out* pr) {
@@ -561,6 +562,13 @@ int cpa_append_kv(const cpa_params* p, const void* k_chunk, const void* v_chunk,
   cudaError_t e = launch_append(k_chunk, v_chunk, *cache, g, ps, hs, sms, (cudaStream_t)stream, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "append");
   return CPA_OK;
+}
+
+int cpa_prepare_chunk(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,
+                      const cpa_kv_cache* cache, cpa_tables* tables, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  return chunk_step_impl(p, q, k_chunk, v_chunk, cache, tables, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                         false);
 }
 
 int cpa_chunk_step(const cpa_params* p, const void* q, const void* k_chunk, const void* v_chunk,

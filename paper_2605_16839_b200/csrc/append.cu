@@ -3,6 +3,7 @@
 #include "../../include/cpa.h"
 #include "common.cuh"
 #include "geo.cuh"
+#include "launch.cuh"
 
 namespace cpa {
 
@@ -10,7 +11,8 @@ namespace cpa {
 // Hkv*d/8 16-byte vectors of K and of V (source [B, C, Hkv, d] contiguous, so every warp request is
 // 512 contiguous bytes; each (head, token) row of d elements lands contiguous in its page slot). All
 // loads of a token are issued before its stores (4 x 2 vectors per lane in flight for d=128, Hkv=8).
-// Grid: at most 8 resident 8-warp CTAs per SM, grid-stride over tokens.
+// Grid: at most 4 resident 8-warp CTAs per SM (half the threads: k_pool_q runs alongside under PDL),
+// grid-stride over tokens.
 constexpr int kAppendUnroll = 4;
 __global__ void __launch_bounds__(256) k_append(const uint4* __restrict__ kc, const uint4* __restrict__ vc,
                                                 uint4* __restrict__ kp, uint4* __restrict__ vp,
@@ -22,6 +24,8 @@ __global__ void __launch_bounds__(256) k_append(const uint4* __restrict__ kc, co
   const long long hs16 = hs >> 3, ps16 = ps >> 3;
   const bool f16 = (g.flags & CPA_F_V_F16) != 0;
   const long long wstride = ((long long)gridDim.x * blockDim.x) >> 5;
+  pdl_wait();     // the pages may still be read by the previous kernel (e.g. the last step's attention)
+  pdl_trigger();  // pool_q (next) does not read the pages: let it run alongside
   for (long long tok = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tok < ntok; tok += wstride) {
     const int b = (int)(tok / g.C);
     const int t = g.P + (int)(tok - (long long)b * g.C);
@@ -64,13 +68,12 @@ cudaError_t launch_append(const void* kc, const void* vc, const cpa_kv_cache& c,
                           long long hs, int num_sms, cudaStream_t st, int* launches) {
   const long long ntok = (long long)g.B * g.C;
   const long long need = (ntok + 7) / 8;         // 8 tokens (warps) per CTA
-  const long long cap = (long long)num_sms * 8;  // 8 resident 256-thread CTAs per SM
+  const long long cap = (long long)num_sms * 4;  // 4 resident 256-thread CTAs per SM (room for pool_q)
   const int blocks = (int)(need < cap ? need : cap);
-  k_append<<<blocks, 256, 0, st>>>(reinterpret_cast<const uint4*>(kc), reinterpret_cast<const uint4*>(vc),
-                                   reinterpret_cast<uint4*>(c.k_pages), reinterpret_cast<uint4*>(c.v_pages),
-                                   c.page_table, g, ps, hs);
   ++*launches;
-  return cudaGetLastError();
+  return launch_ex(k_append, dim3(blocks), dim3(256), 0, st, use_pdl(g), reinterpret_cast<const uint4*>(kc),
+                   reinterpret_cast<const uint4*>(vc), reinterpret_cast<uint4*>(c.k_pages),
+                   reinterpret_cast<uint4*>(c.v_pages), c.page_table, g, ps, hs);
 }
 
 // NEXT-3 "copy" execution ablation: gather the tabled K/V pages of every

@@ -27,6 +27,7 @@
 // 10 TMA producer, 11 TMEM alloc + MMA issuer.
 #include "common.cuh"
 #include "geo.cuh"
+#include "launch.cuh"
 #include "out_store.cuh"
 
 namespace cpa {
@@ -104,6 +105,44 @@ __device__ __forceinline__ void unit_table(const Geo& g, const AttnArgs& args, i
   *start = s;
   *n = e - s;
   *nd = lo - s;
+}
+
+// Number of entries <= key of the ascending list a[0, n), by a whole warp: a 32-ary search, i.e.
+// ceil(log32 n) rounds of dependent loads (2 for n <= 1024) instead of a lane's log2(n) chain (each
+// step an L2 round trip that the cluster's prologue would otherwise wait on).
+__device__ __forceinline__ int warp_count_le(const int32_t* __restrict__ a, int n, int key) {
+  const int lane = (int)lane_id();
+  int lo = 0, hi = n;  // the count c satisfies lo <= c <= hi
+  while (lo < hi) {
+    const int step = (hi - lo + 31) >> 5;
+    const int pos = lo + (lane + 1) * step - 1;
+    const bool le = pos < hi && __ldg(a + pos) <= key;
+    const int k = __popc(__ballot_sync(0xffffffffu, le));  // probes <= key (they ascend)
+    const int nlo = lo + k * step;
+    hi = min(hi, nlo + step - 1);
+    lo = nlo;
+  }
+  return lo;
+}
+
+// unit_table by the whole warp (same results): the visible prefix and its fully visible part.
+__device__ __forceinline__ void unit_table_warp(const Geo& g, const AttnArgs& args, int u, int* start, int* n,
+                                                int* nd) {
+  const Unit c = unit_coords(g, u);
+  const int p0 = c.qt * 128;
+  const int jmax = (g.P + min(p0 + 127, g.C - 1)) / g.bs;
+  const int jfull = (g.P + p0 + 1) / g.bs - 1;
+  if (args.indptr == nullptr) {
+    *start = 0;
+    *n = jmax + 1;
+    *nd = min(jfull + 1, jmax + 1);
+    return;
+  }
+  const int r = c.b * g.Gn + c.grp;
+  const int s = __ldg(args.indptr + r), len = __ldg(args.indptr + r + 1) - s;
+  *start = s;
+  *n = warp_count_le(args.indices + s, len, jmax);
+  *nd = warp_count_le(args.indices + s, *n, jfull);
 }
 
 // Page range [lo, hi) of persistent cluster c in segment s (a segment = the units of one (b, group)
@@ -282,32 +321,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   constexpr uint32_t kConvWarp0 = 8, kTmaWarp = 10, kMmaWarp = 11;
   const bool vf16 = PF16 && (g.flags & (1u << 12)) != 0;  // CPA_F_V_F16: V pages already fp16
 
-  if (warp == kTmaWarp && lane == 0) {
-    tma_prefetch_desc(&tm_q);
-    tma_prefetch_desc(&tm_k_half);
-    tma_prefetch_desc(&tm_v);
-    for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-    for (int s = 0; s < Cfg::kKStages; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
-    for (int s = 0; s < Cfg::kVStages; ++s) {
-      mbar_init(v_full + s, 1);
-      mbar_init(v_empty + s, 1);
-      mbar_init(v_ready + s, 2 * Cfg::kConvWarps);
+  if (warp == kTmaWarp) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k_half);
+      tma_prefetch_desc(&tm_v);
+      for (int i = 0; i < 2; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
+      for (int s = 0; s < Cfg::kKStages; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+      for (int s = 0; s < Cfg::kVStages; ++s) {
+        mbar_init(v_full + s, 1);
+        mbar_init(v_empty + s, 1);
+        mbar_init(v_ready + s, 2 * Cfg::kConvWarps);
+      }
+      mbar_init(s_full, 1);
+      mbar_init(s_full + 1, 1);
+      for (int i = 0; i < 4; ++i) mbar_init(p_full + i, 8);  // 4 softmax warps of WG w x 2 CTAs
+      mbar_init(pv_done, 1);
+      mbar_init(pv_done + 1, 1);
+      mbar_init(o_full, 1);
+      mbar_init(o_empty, 16);  // 8 softmax warps x 2 CTAs
+      for (int i = 0; i < 8; ++i) mbar_init(stag + i, 1);
+      fence_barrier_init();
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_full + 1, 1);
-    for (int i = 0; i < 4; ++i) mbar_init(p_full + i, 8);  // 4 softmax warps of WG w x 2 CTAs
-    mbar_init(pv_done, 1);
-    mbar_init(pv_done + 1, 1);
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 16);  // 8 softmax warps x 2 CTAs
-    for (int i = 0; i < 8; ++i) mbar_init(stag + i, 1);
-    fence_barrier_init();
-    if constexpr (!PERSIST) {  // one cluster = one whole unit
+    __syncwarp();
+    pdl_wait();  // tables (mask_union) complete; the other threads wait at the cluster barrier below
+    if constexpr (!PERSIST) {  // one cluster = one whole unit (its table prefix found by the whole warp)
       int s, n, nd;
-      unit_table(g, args, cl, &s, &n, &nd);
-      single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd;
-      *total_s = n;
-    } else {  // stream-K: share cl of every segment
+      unit_table_warp(g, args, cl, &s, &n, &nd);
+      if (lane == 0) {
+        single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd;
+        *total_s = n;
+      }
+    } else if (lane == 0) {  // stream-K: share cl of every segment
       int total = 0;
       for (int s = 0; s < sk.segments; ++s) {
         int lo, hi;
@@ -321,6 +366,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   tc_fence_before();
   cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
   tc_fence_after();
+  pdl_wait();  // (PDL) every thread: the predecessor's writes (tables) are visible before any access
   const uint32_t tmem = *tmem_slot;
   const int G = *total_s;  // pages this cluster processes (all items)
 
@@ -782,8 +828,8 @@ static cudaError_t launch_2cta_t(const CUtensorMap& tq, const CUtensorMap& tk_ha
       return e;
     ++*launches;
     SkSched none{};
-    kern<<<2 * units, Cfg::kThreads, Cfg::kSmem, st>>>(tq, tk_half, tv, g, a, none);
-    return cudaGetLastError();
+    return launch_ex(kern, dim3(2 * units), dim3(Cfg::kThreads), Cfg::kSmem, st, use_pdl(g), tq, tk_half, tv, g, a,
+                     none);
   }
   using Cfg = Attn2Cfg<BS, true>;
   auto kern = k_paged_attn_2cta<BS, PF16, true>;

@@ -271,6 +271,11 @@ CPA_DEV uint32_t bf16x2_to_f16x2(uint32_t w) {
       : "f"(__uint_as_float(w & 0xffff0000u)), "f"(__uint_as_float(w << 16)));
   return d;
 }
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-stream-serialization
+// attribute may start when its predecessor triggers; pdl_wait() blocks until the predecessor grid has
+// completed and its memory is visible (a no-op without the attribute). launch.cuh launches with it.
+CPA_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+CPA_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 CPA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 CPA_DEV float fast_exp2(float x) {
   float y;

@@ -9,6 +9,7 @@
 // TMEM tile, so the score carries ~2^-16 relative error instead of bf16's 2^-8 (K2).
 #include "common.cuh"
 #include "geo.cuh"
+#include "launch.cuh"
 
 namespace cpa {
 
@@ -24,6 +25,7 @@ __global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict
                                                  unsigned* __restrict__ tables_done) {
   __shared__ float part[kPoolParts - 1][64][9];
   const int i = blockIdx.x, b = blockIdx.y;
+  pdl_trigger();  // block_scores may start its prologue; it waits for this grid before reading qbar
   if (i == 0 && b == 0 && blockIdx.z == 0 && threadIdx.x == 0) *tables_done = 0u;  // k_mask_union's counter
   const long long nrows = (long long)g.B * g.Gn * g.Rpad;
   if (i == g.nqb) {  // padding rows of the groups z, z + gridDim.z, ... of batch b
@@ -35,6 +37,7 @@ __global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict
         *reinterpret_cast<uint4*>(qbar + row * g.d + e) = make_uint4(0u, 0u, 0u, 0u);
         *reinterpret_cast<uint4*>(qbar + (nrows + row) * g.d + e) = make_uint4(0u, 0u, 0u, 0u);
       }
+    pdl_wait();  // this grid completes only after its predecessor (the append of the chunk's K/V)
     return;
   }
   const int st = threadIdx.x & 63, pt = threadIdx.x >> 6;
@@ -68,6 +71,7 @@ __global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict
     for (int c = 0; c < 8; ++c) part[pt - 1][st][c] = acc[c];
   }
   __syncthreads();
+  pdl_wait();  // this grid completes only after its predecessor (the append of the chunk's K/V)
   if (pt != 0 || !active) return;
   for (int k = 0; k < kPoolParts - 1; ++k)
 #pragma unroll
@@ -141,6 +145,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // mask_union may be scheduled (it waits for this grid)
+  pdl_wait();     // qbar / row-max init (pool_q) and the appended K pages are complete
 
   // TMA / MMA roles: whole warp runs the loop (warp-uniform values live in uniform registers),
   // one elected lane issues each TMA / tcgen05 instruction.
@@ -468,12 +474,12 @@ int score_smem_bytes(int d, int bs) {
 }
 
 cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* qbar, int* mstar_key,
-                          unsigned* tables_done, cudaStream_t st, int* launches) {
-  // x = nqb: padding blocks (they return at once when Rpad == R)
-  k_pool_q<<<dim3(g.nqb + (g.Rpad > g.R ? 1 : 0), g.B, (g.Hq * g.d + 511) / 512), 1024, 0, st>>>(q, g, qbar, mstar_key,
-                                                                                                tables_done);
+                          unsigned* tables_done, bool after_append, cudaStream_t st, int* launches) {
+  // x = nqb: padding blocks (they return at once when Rpad == R). PDL only right after k_append (whose
+  // pdl_wait orders it after everything before): then q, qbar and the counters are safe to touch early.
   ++*launches;
-  return cudaGetLastError();
+  return launch_ex(k_pool_q, dim3(g.nqb + (g.Rpad > g.R ? 1 : 0), g.B, (g.Hq * g.d + 511) / 512), dim3(1024), 0, st,
+                   after_append && use_pdl(g), q, g, qbar, mstar_key, tables_done);
 }
 
 template <int D, int BS>
@@ -490,9 +496,8 @@ static cudaError_t launch_scores_t(const CUtensorMap& tq, const CUtensorMap& tk,
   if (splits > g.nkvb) splits = g.nkvb;
   const int ppc = (g.nkvb + splits - 1) / splits;
   splits = (g.nkvb + ppc - 1) / ppc;
-  kern<<<dim3(splits, g.Rpad / 128, g.B * g.Gn), 192, Cfg::kSmem, st>>>(tq, tk, pt, g, ppc, scores,
-                                                                         mstar_key);
-  return cudaGetLastError();
+  return launch_ex(kern, dim3(splits, g.Rpad / 128, g.B * g.Gn), dim3(192), Cfg::kSmem, st, use_pdl(g), tq, tk, pt, g,
+                   ppc, scores, mstar_key);
 }
 
 cudaError_t launch_block_scores(const CUtensorMap& tq, const CUtensorMap& tk, const int32_t* pt,

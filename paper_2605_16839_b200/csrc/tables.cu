@@ -8,6 +8,7 @@
 //                  SPEC.md:305-311, 343)
 #include "common.cuh"
 #include "geo.cuh"
+#include "launch.cuh"
 
 namespace cpa {
 
@@ -77,6 +78,8 @@ __global__ void __launch_bounds__(128)
   const int w = blockIdx.x, bg = blockIdx.y;
   const int b = bg / g.Gn, grp = bg % g.Gn;
   const bool sink = (g.flags & 1u) != 0;
+  pdl_wait();     // scores / row max (block_scores) or mask_in complete
+  pdl_trigger();  // the attention may start its prologue (it waits for this grid before the tables)
   const int jbase = w * 32;
   // valid kv blocks of this word: j < nkvb
   const int nvalid = min(32, g.nkvb - jbase);
@@ -140,10 +143,9 @@ cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& 
                           const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
                           int* dev_status, unsigned* done, int32_t* indptr, int32_t* indices, cudaStream_t st,
                           int* launches) {
-  k_mask_union<<<dim3(g.nwords, g.B * g.Gn), 128, 0, st>>>(scores, mstar_key, g, mask_in, mask_out,
-                                                           gwords, dev_status, done, indptr, indices);
   *launches += 1;
-  return cudaGetLastError();
+  return launch_ex(k_mask_union, dim3(g.nwords, g.B * g.Gn), dim3(128), 0, st, use_pdl(g), scores, mstar_key, g,
+                   mask_in, mask_out, gwords, dev_status, done, indptr, indices);
 }
 
 // Fig. 7(c) ablation ("the same unioned block mask"; SPEC.md:447 q-uniform expansion):

@@ -61,8 +61,7 @@ def _bench_step(cfg_name):
         tables.kv_indices.fill_(-1)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            cpa.append_kv(p, kc, vc, cache)
-            cpa.build_tables(p, dq, cache, tables, workspace=ws)
+            cpa.prepare_chunk(p, dq, cache, tables, kc, vc, workspace=ws)
             cpa.paged_attention(p, dq, cache, tables, o, workspace=ws)
         g.replay()
         g.replay()
@@ -98,7 +97,7 @@ def test_every_row_bench_config(cfg_name):
     stats = {"config": cfg_name, "outputs": int(ref.size), "rms": rms, "max_abs_err_over_rms_f32": err32,
              "mean_abs_err_over_rms_f32": float(d32.mean()) / rms, "max_abs_err_over_rms_bf16": err16,
              "bf16_bound_ratio": ratio16, "tabled_blocks": int(ip[-1]), "oracle_wall_s": round(t_oracle, 1),
-             "launch": "CUDA graph replay of append + build_tables + paged_attention, fp16 V pool"}
+             "launch": "CUDA graph replay of prepare_chunk (append + estimator + tables) + paged_attention, fp16 V pool"}
     print(json.dumps(stats))
     out_dir = os.environ.get("CPA_PARITY_OUT")
     if out_dir:
