@@ -401,6 +401,9 @@ def run_gpu(args):
     del k, v
     E_exec = args.exec_group or E
     vflag = cpa.F_V_F16 if args.v_f16 else 0
+    if os.environ.get("CPA_BENCH_NO_PDL") == "1":  # A/B only: launch the chain without PDL
+        vflag |= cpa.F_NO_PDL
+    vflag |= int(os.environ.get("CPA_BENCH_EXTRA_FLAGS", "0"))  # A/B only (e.g. CPA_F_ATTN_V1)
     sflag = cpa.F_EXACT_SCORES if args.exact_scores else 0
     p = cpa.make_params(cfg.batch, hq_l, hkv_l, d, bs, C, P, alpha=ALPHA, exec_group_size=args.exec_group,
                         flags=sflag | vflag)

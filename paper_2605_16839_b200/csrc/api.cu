@@ -28,6 +28,9 @@ cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& 
 cudaError_t launch_paged_attention(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                                    const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 bool attn_2cta_supported(const Geo& g);
+bool attn_rs_supported(const Geo& g);
+cudaError_t launch_paged_attention_rs(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
+                                      const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 int attn_2cta_max_clusters(const Geo& g);
 cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
                                         const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st,
@@ -370,7 +373,7 @@ struct OutSpec {
 struct AttnPlan {
   CUtensorMap tq, tk, tv, tkh;
   AttnArgs a;
-  int kind;  // 0: 1-CTA kernel, 1: 2-CTA per-unit grid, 2: 2-CTA persistent stream-K grid
+  int kind;  // 0: 1-CTA kernel, 1: 2-CTA per-unit grid, 2: 2-CTA persistent stream-K grid, 3: row-split 2-CTA
   SkSched sk;
 };
 
@@ -415,6 +418,7 @@ int prep_attention(const cpa_params* p, const Geo& g, const void* q, const void*
       ap->sk = carve_sk(g, ws, clusters);
       ap->kind = 2;
     }
+    if (ap->kind == 1 && attn_rs_supported(g) && (p->flags & CPA_F_ATTN_RS)) ap->kind = 3;
   }
   return CPA_OK;
 }
@@ -422,6 +426,7 @@ int prep_attention(const cpa_params* p, const Geo& g, const void* q, const void*
 int run_attention(const Geo& g, const AttnPlan& ap, cudaStream_t st) {
   cudaError_t e;
   if (ap.kind == 0) e = launch_paged_attention(ap.tq, ap.tk, ap.tv, g, ap.a, st, &g_launches);
+  else if (ap.kind == 3) e = launch_paged_attention_rs(ap.tq, ap.tkh, ap.tv, g, ap.a, st, &g_launches);
   else e = launch_paged_attention_2cta(ap.tq, ap.tkh, ap.tv, g, ap.a, ap.kind == 2 ? &ap.sk : nullptr, st, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "paged_attention");
   return CPA_OK;

@@ -897,6 +897,386 @@ cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap
   return cudaErrorInvalidValue;
 }
 
+
+// ================================================================================================
+// Row-split variant (default for d = 128, bs = 128, even E, per-unit grid): the same cluster pair
+// and M=256 MMAs, but the 8 softmax warps split the CTA's 128 query rows instead of each page's keys:
+// warp w owns TMEM lanes (rows) [32(w%4) + 16(w/4), +16) and all 128 keys of every page, accessed
+// with the 16-lane tcgen05.ld/st shapes (16x256b: thread t holds rows t/4 and t/4+8, column pairs
+// 8r + 2(t%4) + {0,1}; P is stored with 16x128b, column 4r + t%4 = the fp16 pair of those keys). Each
+// row has ONE running max, so both warps' P.V accumulate into a single O, and the 128 TMEM columns
+// this frees hold a third S buffer:
+//   TMEM per CTA: S^0 [0,128) S^1 [128,256) S^2 [256,384) O [384,512).
+// S(n+3) is issued right after P.V(n) (in-order tensor pipe), so the softmax of page n+1 never waits
+// for the P.V of page n; the tensor core has a full page of slack (with two buffers S(n+2) had to wait
+// for the lagging warpgroup's P(n)). Row max over a page = 32 values per thread plus
+// two xor-shuffles across the row's 4 threads; the row sum is a per-thread partial reduced at the end.
+// Warps: 0-7 softmax, 8-9 V bf16 -> fp16 converters (bf16 pool only), 10 TMA producer, 11 TMEM alloc +
+// MMA issuer (CTA 0 issues for the pair).
+struct AttnRsCfg {
+  static constexpr int BS = 128, D = 128;
+  static constexpr int kQBytes = 128 * D * 2;
+  static constexpr int kKHalf = (BS / 2) * D * 2;  // keys [r*64, r*64+64) of a page
+  static constexpr int kVHalf = BS * 64 * 2;       // head-dim columns [64r, 64r+64) of a page
+  static constexpr int kKStages = 4, kVStages = 4;
+  static constexpr int kConvWarps = 2;
+  static constexpr int kThreads = 12 * 32;
+  static constexpr int kSmem = kQBytes + kKStages * kKHalf + kVStages * kVHalf + 1024 + 1024;
+  static_assert(kSmem + 2048 <= 232448, "shared memory budget");
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    k_paged_attn_rs(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k_half,
+                    const __grid_constant__ CUtensorMap tm_v, Geo g, AttnArgs args) {
+  using Cfg = AttnRsCfg;
+  constexpr int D = Cfg::D, BS = Cfg::BS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Cfg::kQBytes;
+  uint8_t* sV = sK + Cfg::kKStages * Cfg::kKHalf;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::kVStages * Cfg::kVHalf);
+  uint64_t* q_full = bars;                          // leader: both Q tiles landed (tx)
+  uint64_t* k_full = q_full + 1;                    // leader: both K halves landed (tx)
+  uint64_t* k_empty = k_full + Cfg::kKStages;       // both: K stage consumed (multicast commit)
+  uint64_t* v_full = k_empty + Cfg::kKStages;       // leader (fp16 pool: both halves, tx) / local (bf16)
+  uint64_t* v_empty = v_full + Cfg::kVStages;       // both: V stage consumed (multicast commit)
+  uint64_t* v_ready = v_empty + Cfg::kVStages;      // leader: both V halves converted (bf16 pool)
+  uint64_t* s_full = v_ready + Cfg::kVStages;       // both [3]: S^b computed (multicast commit)
+  uint64_t* p_full = s_full + 3;                    // leader [3]: P^b written by all 16 softmax warps
+  uint64_t* pv_done = p_full + 3;                   // both [2]: P.V of a page of that parity complete
+  uint64_t* o_full = pv_done + 2;                   // both: every MMA of the unit complete
+  uint64_t* stag = o_full + 1;                      // local [4 quarters][4]: warp q done with page max
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stag + 16);
+  int* single_s = reinterpret_cast<int*>(tmem_slot + 1);  // {unit, start, n, nd}
+  float* l_s = reinterpret_cast<float*>(single_s + 4);    // [128] row sums for the epilogue
+
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int cl = (int)blockIdx.x >> 1;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  constexpr uint32_t kConvWarp0 = 8, kTmaWarp = 10, kMmaWarp = 11;
+  const bool vf16 = (g.flags & (1u << 12)) != 0;  // CPA_F_V_F16: V pages already fp16
+
+  if (warp == kTmaWarp) {
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k_half);
+      tma_prefetch_desc(&tm_v);
+      mbar_init(q_full, 1);
+      for (int s = 0; s < Cfg::kKStages; ++s) { mbar_init(k_full + s, 1); mbar_init(k_empty + s, 1); }
+      for (int s = 0; s < Cfg::kVStages; ++s) {
+        mbar_init(v_full + s, 1);
+        mbar_init(v_empty + s, 1);
+        mbar_init(v_ready + s, 2 * Cfg::kConvWarps);
+      }
+      for (int b = 0; b < 3; ++b) { mbar_init(s_full + b, 1); mbar_init(p_full + b, 16); }
+      mbar_init(pv_done, 1);
+      mbar_init(pv_done + 1, 1);
+      mbar_init(o_full, 1);
+      for (int i = 0; i < 16; ++i) mbar_init(stag + i, 1);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    pdl_wait();  // tables complete; the other threads wait at the cluster barrier below
+    int s, n, nd;
+    unit_table_warp(g, args, cl, &s, &n, &nd);
+    if (lane == 0) { single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd; }
+  }
+  if (warp == kMmaWarp) tmem_alloc2<512>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();  // barriers initialised, TMEM allocated in both CTAs
+  tc_fence_after();
+  pdl_wait();
+  const uint32_t tmem = *tmem_slot;
+  const int G = single_s[2];  // pages of this unit
+  const Unit uc = unit_coords(g, cl);
+
+  if (warp == kTmaWarp) {
+    if (G > 0) {  // ------------------------------------------------------------ TMA producer
+      const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;
+      const int kvh = group_kv_head(g, uc.grp);
+      if (elect_one()) {
+        if (leader) mbar_expect_tx(q_full, 2 * Cfg::kQBytes);
+        tma_load_4d_2sm(sQ, &tm_q, q_full, 0, h, uc.qt * 128, uc.b);
+        tma_load_4d_2sm(sQ + 128 * 128, &tm_q, q_full, 64, h, uc.qt * 128, uc.b);
+      }
+      __syncwarp();
+      const int32_t* ptab = args.page_table + (long long)uc.b * g.maxb;
+      const int st = single_s[1];
+      for (int t = 0; t < G; ++t) {
+        const int j = args.indptr != nullptr ? __ldg(args.indices + st + t) : t;
+        const int page = __ldg(ptab + j);
+        const int ks = t % Cfg::kKStages, vs = t % Cfg::kVStages;
+        mbar_wait(k_empty + ks, ((t / Cfg::kKStages) & 1) ^ 1);
+        if (elect_one()) {
+          if (leader) mbar_expect_tx(k_full + ks, 2 * Cfg::kKHalf);
+          uint8_t* dst = sK + ks * Cfg::kKHalf;
+          tma_load_4d_2sm(dst, &tm_k_half, k_full + ks, 0, (int)cta * (BS / 2), kvh, page);
+          tma_load_4d_2sm(dst + (BS / 2) * 128, &tm_k_half, k_full + ks, 64, (int)cta * (BS / 2), kvh, page);
+        }
+        __syncwarp();
+        mbar_wait(v_empty + vs, ((t / Cfg::kVStages) & 1) ^ 1);
+        if (elect_one()) {
+          if (vf16) {  // both halves signal the leader's v_full directly
+            if (leader) mbar_expect_tx(v_full + vs, 2 * Cfg::kVHalf);
+            tma_load_4d_2sm(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+          } else {
+            mbar_expect_tx(v_full + vs, Cfg::kVHalf);
+            tma_load_4d(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    if (leader && G > 0) {  // ---------------------------------------------------- MMA issuer (CTA 0)
+      constexpr uint32_t idesc_s = umma_idesc_bf16(256, BS, 0, 0);
+      constexpr uint32_t idesc_o = umma_idesc_bf16(256, D, 0, 1) & ~((7u << 7) | (7u << 10));  // fp16 A/B
+      const uint32_t q_base = smem_u32(sQ), k_base = smem_u32(sK), v_base = smem_u32(sV);
+      auto wait_k = [&](int n) {
+        mbar_wait(k_full + n % Cfg::kKStages, (n / Cfg::kKStages) & 1);
+        tc_fence_after();
+      };
+      auto issue_s = [&](int n) {  // S^{n%3} = Q K_n^T, M=256 (both CTAs' rows), N=BS, K=d
+        const uint32_t d_tm = tmem + (n % 3) * 128;
+        const uint32_t kb = k_base + (n % Cfg::kKStages) * Cfg::kKHalf;
+        if (elect_one()) {
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t ad = umma_desc_sw128(q_base + a * 128 * 128 + kk * 32, 16, 1024);
+              const uint64_t bd = umma_desc_sw128(kb + a * (BS / 2) * 128 + kk * 32, 16, 1024);
+              mma2_ss(d_tm, ad, bd, idesc_s, (a | kk) != 0);
+            }
+          tc_commit2(s_full + n % 3);
+          tc_commit2(k_empty + n % Cfg::kKStages);
+        }
+        __syncwarp();
+      };
+      mbar_wait(q_full, 0);
+      tc_fence_after();
+      for (int n = 0; n < 3 && n < G; ++n) {
+        wait_k(n);
+        issue_s(n);
+      }
+      for (int n = 0; n < G; ++n) {
+        mbar_wait((vf16 ? v_full : v_ready) + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
+        mbar_wait(p_full + n % 3, (n / 3) & 1);
+        tc_fence_after();
+        // O += P^{n%3} V_n: M=256, N=d (64 columns per CTA), K=BS keys (P fp16 pairs over S^b [0, 64))
+        const uint32_t p_tm = tmem + (n % 3) * 128;
+        const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kVHalf;
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BS / 16; ++kk) {
+            const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
+            mma2_ts(tmem + 384, p_tm + kk * 8, bd, idesc_o, (n > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit2(pv_done + (n & 1));
+          tc_commit2(v_empty + n % Cfg::kVStages);
+          if (n + 1 == G) tc_commit2(o_full);
+        }
+        __syncwarp();
+        if (n + 3 < G) {  // S^{n%3} is free once P.V(n) (issued just before, in-order pipe) has read it
+          wait_k(n + 3);
+          issue_s(n + 3);
+        }
+      }
+    }
+  } else if (warp >= kConvWarp0) {  // --------------------------------------- V bf16 -> fp16
+    const int ct = (warp - kConvWarp0) * 32 + lane;
+    for (int n = 0; n < (vf16 ? 0 : G); ++n) {
+      const int vs = n % Cfg::kVStages;
+      mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
+      constexpr int kPer = Cfg::kVHalf / 16 / (Cfg::kConvWarps * 32);
+      uint4* tile = reinterpret_cast<uint4*>(sV + vs * Cfg::kVHalf);
+      uint4 w[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) w[i] = tile[ct + i * Cfg::kConvWarps * 32];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        w[i].x = bf16x2_to_f16x2(w[i].x);
+        w[i].y = bf16x2_to_f16x2(w[i].y);
+        w[i].z = bf16x2_to_f16x2(w[i].z);
+        w[i].w = bf16x2_to_f16x2(w[i].w);
+        tile[ct + i * Cfg::kConvWarps * 32] = w[i];
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(v_ready + vs, 0);
+    }
+  } else {  // ------------------------------------------------------------------ softmax / epilogue
+    const int quarter = warp & 3, hf = warp >> 2;
+    const int base = quarter * 32 + hf * 16;  // this warp's 16 rows (TMEM lanes)
+    const int t0 = lane & 3, t1 = lane >> 2;
+    const int ra = base + t1, rb = ra + 8;    // the thread's two rows
+    const float sl2 = g.scale * 1.4426950408889634f;
+    const uint32_t lane_off = (uint32_t)base << 16;
+    const int p0 = uc.qt * 128;
+    const int lim_a = min(g.P + p0 + ra, g.L - 1), lim_b = min(g.P + p0 + rb, g.L - 1);
+    const int st = single_s[1], nd = single_s[3];
+    float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+    for (int t = 0; t < G; ++t) {
+      const int b = t % 3;
+#ifndef CPA_NO_STAGGER
+      // the two warps of an SMSP (same quarter): the second starts a page once the first has its max
+      if (hf == 1) mbar_wait(stag + quarter * 4 + (t & 3), (t >> 2) & 1);
+#endif
+      mbar_wait(s_full + b, (t / 3) & 1);
+      tc_fence_after();
+      uint32_t sv[64];
+      tmem_ld_16x256b_x16(tmem + lane_off + b * 128, sv);
+      tmem_wait_ld();
+      if (t >= nd) {  // block crosses the causal diagonal of this tile: mask in absolute positions
+        const int j = args.indptr != nullptr ? __ldg(args.indices + st + t) : t;
+        const int tb = j * g.bs + 2 * t0;
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (tb + 8 * r + e > lim_a) sv[4 * r + e] = __float_as_uint(-INFINITY);
+            if (tb + 8 * r + e > lim_b) sv[4 * r + 2 + e] = __float_as_uint(-INFINITY);
+          }
+      }
+      float ma0 = -INFINITY, ma1 = -INFINITY, mb0 = -INFINITY, mb1 = -INFINITY;
+#pragma unroll
+      for (int r = 0; r < 16; r += 2) {
+        ma0 = fmax3(ma0, __uint_as_float(sv[4 * r]), __uint_as_float(sv[4 * r + 1]));
+        ma1 = fmax3(ma1, __uint_as_float(sv[4 * r + 4]), __uint_as_float(sv[4 * r + 5]));
+        mb0 = fmax3(mb0, __uint_as_float(sv[4 * r + 2]), __uint_as_float(sv[4 * r + 3]));
+        mb1 = fmax3(mb1, __uint_as_float(sv[4 * r + 6]), __uint_as_float(sv[4 * r + 7]));
+      }
+      float mxa = fmaxf(ma0, ma1), mxb = fmaxf(mb0, mb1);
+      mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 1));
+      mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 1));
+      mxa = fmaxf(mxa, __shfl_xor_sync(0xffffffffu, mxa, 2));
+      mxb = fmaxf(mxb, __shfl_xor_sync(0xffffffffu, mxb, 2));
+      const float mba = mxa * sl2, mbb = mxb * sl2;
+      float fa = 1.f, fb = 1.f;
+      const bool ra_s = mba > m_a + CPA_RESCALE_THRESH, rb_s = mbb > m_b + CPA_RESCALE_THRESH;  // lazy rescale
+      if (ra_s) {
+        if (m_a != -INFINITY) fa = fast_exp2(m_a - mba);
+        m_a = mba;
+      }
+      if (rb_s) {
+        if (m_b != -INFINITY) fb = fast_exp2(m_b - mbb);
+        m_b = mbb;
+      }
+      const float ua = (m_a == -INFINITY) ? 0.f : m_a, ub = (m_b == -INFINITY) ? 0.f : m_b;
+#ifndef CPA_NO_STAGGER
+      if (hf == 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stag + quarter * 4 + (t & 3));
+      }
+#endif
+      // P = exp2(s*sl2 - m) per row: packed FFMA2 on each column pair, 1/4 of the pairs on the FMA-pipe
+      // polynomial, the rest on MUFU.EX2; fp16 pairs stored over S^b columns [0, 64) (16x128b).
+      float2 acc_a = {0.f, 0.f}, acc_b = {0.f, 0.f};
+      uint32_t pk[32];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const float2 xa = ffma2(make_float2(__uint_as_float(sv[4 * r]), __uint_as_float(sv[4 * r + 1])), sl2, -ua);
+        const float2 xb = ffma2(make_float2(__uint_as_float(sv[4 * r + 2]), __uint_as_float(sv[4 * r + 3])), sl2, -ub);
+        float2 ea, eb;
+        if (use_poly_exp(2 * r)) {
+          ea = exp2_poly2(xa);
+        } else {
+          ea.x = fast_exp2(xa.x);
+          ea.y = fast_exp2(xa.y);
+        }
+        if (use_poly_exp(2 * r + 1)) {
+          eb = exp2_poly2(xb);
+        } else {
+          eb.x = fast_exp2(xb.x);
+          eb.y = fast_exp2(xb.y);
+        }
+        acc_a = fadd2(acc_a, ea);
+        acc_b = fadd2(acc_b, eb);
+        pk[2 * r] = pack_f16x2(ea.x, ea.y);
+        pk[2 * r + 1] = pack_f16x2(eb.x, eb.y);
+      }
+      tmem_st_16x128b_x16(tmem + lane_off + b * 128, pk);
+      l_a = l_a * fa + (acc_a.x + acc_a.y);
+      l_b = l_b * fb + (acc_b.x + acc_b.y);
+      // rescale O's rows (this warp's 16) after the previous P.V completed, before P.V(t) is issued;
+      // not on the first page (its P.V overwrites O). pv_done[x] completes once per page of parity x and
+      // P.V(t-3) is complete here (S(t) was issued after it), so its phase is known within one.
+      if (__any_sync(0xffffffffu, (ra_s || rb_s) && t > 0)) {
+        mbar_wait(pv_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
+        tc_fence_after();
+        uint32_t o[64];
+        tmem_ld_16x256b_x16(tmem + lane_off + 384, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          o[4 * r] = __float_as_uint(__uint_as_float(o[4 * r]) * fa);
+          o[4 * r + 1] = __float_as_uint(__uint_as_float(o[4 * r + 1]) * fa);
+          o[4 * r + 2] = __float_as_uint(__uint_as_float(o[4 * r + 2]) * fb);
+          o[4 * r + 3] = __float_as_uint(__uint_as_float(o[4 * r + 3]) * fb);
+        }
+        tmem_st_16x256b_x16(tmem + lane_off + 384, o);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(p_full + b, 0);
+    }
+    // ---- epilogue: O / l. Row sums: reduce the row's 4 partials, exchange through shared memory so
+    // that warp (q, hf) stores output columns [64 hf, 64 hf + 64) of the quarter's 32 rows (32x32b).
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 1);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 1);
+    l_a += __shfl_xor_sync(0xffffffffu, l_a, 2);
+    l_b += __shfl_xor_sync(0xffffffffu, l_b, 2);
+    if (t0 == 0) {
+      l_s[ra] = l_a;
+      l_s[rb] = l_b;
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // warps q and q+4
+    const int row = quarter * 32 + lane;
+    const float lt = l_s[row];
+    const float inv = lt > 0.f ? 1.0f / lt : 0.f;
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;
+    const int p = p0 + row;
+    const long long obase = (long long)uc.b * args.o_bstride + (long long)p * args.o_stride + (long long)h * D + hf * 64;
+    const uint32_t ob = tmem + ((uint32_t)(quarter * 32) << 16) + 384 + hf * 64;
+#pragma unroll
+    for (int cc = 0; cc < 64; cc += 32) {
+      uint32_t o[32];
+      tmem_ld32(ob + cc, o);  // warp-collective: every lane, valid row or not
+      tmem_wait_ld();
+      float v[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(o[c]) * inv;
+      if (p < g.C) store_o_row32(args, obase + cc, v);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // no CTA leaves while the pair's MMAs / remote arrivals may still touch it
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc2<512>(tmem);
+  }
+}
+
+bool attn_rs_supported(const Geo& g) { return g.d == 128 && g.bs == 128 && g.E % 2 == 0 && !(g.flags & (1u << 8)); }
+
+cudaError_t launch_paged_attention_rs(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
+                                      const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches) {
+  using Cfg = AttnRsCfg;
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_paged_attn_rs, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem)) !=
+      cudaSuccess)
+    return e;
+  const int units = (g.C + 127) / 128 * g.B * g.Gn * (g.E / 2);
+  ++*launches;
+  return launch_ex(k_paged_attn_rs, dim3(2 * units), dim3(Cfg::kThreads), Cfg::kSmem, st, use_pdl(g), tq, tk_half, tv,
+                   g, a);
+}
+
 }  // namespace cpa
 
 #ifdef CPA_TRACE

@@ -68,8 +68,8 @@ __device__ void csr_block(const uint32_t* gwords, const Geo& g, int32_t* indptr,
 
 // One CTA per (word w of 32 kv blocks, execution group bg). Thread t handles estimator rows
 // r = t, t+blockDim, ... (r = hl*nqb + i). Each row forms its 32-bit mask word, the CTA ORs the
-// words of all its rows (Q-block union and intra-group union in one reduction). The last CTA to
-// finish (device-scope counter `done`, zero on entry and reset on exit) builds the CSR tables.
+// words of all its rows (Q-block union and intra-group union in one reduction). The CSR tables are
+// built by k_csr (next kernel, one 1024-thread CTA, PDL-overlapped with this one).
 __global__ void __launch_bounds__(128)
     k_mask_union(const float* __restrict__ scores, const int* __restrict__ mstar_key, Geo g,
                  const uint32_t* __restrict__ mask_in, uint32_t* __restrict__ mask_out,
@@ -115,7 +115,6 @@ __global__ void __launch_bounds__(128)
   }
   acc = __reduce_or_sync(0xffffffffu, acc);
   __shared__ uint32_t red[32];
-  __shared__ bool last;
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -129,23 +128,27 @@ __global__ void __launch_bounds__(128)
         if (jbase + jj >= g.pb) need |= 1u << jj;
       if ((word & need) != need) atomicCAS(dev_status, 0, 1 + bg);
     }
-    __threadfence();  // publish the word before counting this CTA as done
-    last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
   }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
+}
+
+// a5: CSR of the G words, one CTA (csr_block), after k_mask_union (PDL: resident early, waits for it).
+__global__ void __launch_bounds__(1024) k_csr(const uint32_t* __restrict__ gwords, Geo g, int32_t* __restrict__ indptr,
+                                              int32_t* __restrict__ indices) {
+  pdl_wait();
+  pdl_trigger();
   csr_block(gwords, g, indptr, indices);
-  if (threadIdx.x == 0) *done = 0u;  // ready for the next call
 }
 
 cudaError_t launch_tables(const float* scores, const int* mstar_key, const Geo& g,
                           const uint32_t* mask_in, uint32_t* mask_out, uint32_t* gwords,
                           int* dev_status, unsigned* done, int32_t* indptr, int32_t* indices, cudaStream_t st,
                           int* launches) {
-  *launches += 1;
-  return launch_ex(k_mask_union, dim3(g.nwords, g.B * g.Gn), dim3(128), 0, st, use_pdl(g), scores, mstar_key, g,
-                   mask_in, mask_out, gwords, dev_status, done, indptr, indices);
+  (void)done;
+  *launches += 2;
+  cudaError_t e = launch_ex(k_mask_union, dim3(g.nwords, g.B * g.Gn), dim3(128), 0, st, use_pdl(g), scores, mstar_key,
+                            g, mask_in, mask_out, gwords, dev_status, done, indptr, indices);
+  if (e != cudaSuccess) return e;
+  return launch_ex(k_csr, dim3(1), dim3(1024), 0, st, use_pdl(g), (const uint32_t*)gwords, g, indptr, indices);
 }
 
 // Fig. 7(c) ablation ("the same unioned block mask"; SPEC.md:447 q-uniform expansion):

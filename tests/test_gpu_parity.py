@@ -535,3 +535,27 @@ def test_v_beyond_fp16_range_saturates(pool):
     ip, ix = tables_to_numpy(t)
     ref = O.paged_attention(q, k, np.clip(v, -65504.0, 65504.0), P, bs, ip, ix)
     assert rel_err(got, ref) <= ATOL_REL
+
+
+@pytest.mark.parametrize("flag", [0, cpa.F_ATTN_RS])
+@pytest.mark.parametrize("C,P,density", [(256, 8 * 128, 0.05), (200, 384, 1.0), (130, 1024, 0.3)])
+def test_attention_row_split_and_key_split_kernels(flag, C, P, density):
+    """The two 2-CTA kernels for d=128 / bs=128 -- key-split (default: two O accumulators merged at the
+    end) and row-split (CPA_F_ATTN_RS: one O, three S buffers) -- each against the oracle on
+    random tables (incl. partial q-tiles and the causal diagonal), both V pools."""
+    B, Hq, Hkv, d, bs = 2, 8, 2, 128, 128
+    q, k, v = random_qkv(B, Hq, Hkv, d, C, P + C, seed=C + P)
+    for vf16 in (False, True):
+        case = Case(q, k, v, P, bs, seed=9, flags=flag | (cpa.F_V_F16 if vf16 else 0))
+        if vf16:
+            case.cache = cpa.PagedKVCache(case.cache.k_pages, case.cache.v_pages.half(), case.cache.page_table)
+        nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+        M = random_block_mask(B, Hq, nqb, nkvb, density, seed=C)
+        for i in range(nqb):
+            M[:, :, i, pb + i + 1:] = False
+            M[:, :, i, pb:pb + i + 1] = True
+        ip, ix = O.tables_from_mask(M, case.E, pb)
+        t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
+        got = _gpu_attn(case, t)
+        ref = O.paged_attention(q, k, v, P, bs, ip, ix)
+        assert rel_err(got, ref) <= ATOL_REL, (flag, vf16)
