@@ -40,9 +40,9 @@ for r in range(rounds):
         p.flags = (p.flags & 1) | fl | (cpa.F_V_F16 if VF16 else 0)
         if tabs is None:
             tabs = cpa.alloc_tables(p); cpa.build_tables(p, dq, cache, tabs)
-        for name, tab in (("sparse", tabs), ("dense", None)):
+        for name, tab in (("sparse", tabs),) + ((("dense", None),) if os.environ.get("DENSE", "1") == "1" else ()):
             cpa.paged_attention(p, dq, cache, tab, o)
-            for _ in range(3):
+            for _ in range(int(os.environ.get("REPS", "3"))):
                 flush.zero_(); a = torch.cuda.Event(True); b = torch.cuda.Event(True)
                 a.record(); cpa.paged_attention(p, dq, cache, tab, o); b.record(); torch.cuda.synchronize()
                 times[((path, fl), name)].append(a.elapsed_time(b))
@@ -53,5 +53,7 @@ for r in range(rounds):
 for (path, fl) in variants:
     print(json.dumps({"lib": os.path.basename(path), "flags": fl,
                       "sparse_ms": round(float(np.median(times[((path, fl), "sparse")])), 4),
+                      "sparse_mean_ms": round(float(np.mean(times[((path, fl), "sparse")])), 4),
+                      "sparse_p25_ms": round(float(np.percentile(times[((path, fl), "sparse")], 25)), 4),
                       "sparse_min_ms": round(float(np.min(times[((path, fl), "sparse")])), 4),
-                      "dense_ms": round(float(np.median(times[((path, fl), "dense")])), 4)}), flush=True)
+                      "dense_ms": round(float(np.median(times[((path, fl), "dense")] or [0])), 4)}), flush=True)

@@ -51,16 +51,22 @@ def main():
             o = torch.empty(cfg.batch, C, len(qh), d, dtype=torch.bfloat16, device="cuda")
             for _ in range(3):
                 cpa.chunk_step(p, q, cache, t, o, kc, vc, workspace=ws)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()  # the step as bench.py times it: one graph replay
+            with torch.cuda.graph(g):
+                cpa.chunk_step(p, q, cache, t, o, kc, vc, workspace=ws)
+            g.replay()
             ts = []
             for _ in range(args.reps):
                 flush.zero_()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record()
-                cpa.chunk_step(p, q, cache, t, o, kc, vc, workspace=ws)
+                g.replay()
                 b.record()
                 torch.cuda.synchronize()
                 ts.append(a.elapsed_time(b))
             res[name] = float(np.median(ts))
+            del g
         if t1 is None:
             t1 = res["auto"]
         print(json.dumps({"config": cfg.name, "W": W, "kv_groups_per_gpu": len(kvh), "step_ms": round(res["auto"], 4),
