@@ -712,6 +712,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       xml[wg][1][row] = l_run;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");  // warps q and q+4
       const float m0 = xml[0][0][row], l0 = xml[0][1][row], m1 = xml[1][0][row], l1 = xml[1][1][row];
+      // (persistent grid: xml is rewritten by the next item's epilogue; the mbarrier chain already orders
+      // that after these reads, this barrier makes it explicit for the race checker)
+      if constexpr (PERSIST) asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
       const float mm = fmaxf(m0, m1);
       const float a0 = l0 > 0.f ? fast_exp2(m0 - mm) : 0.f, a1 = l1 > 0.f ? fast_exp2(m1 - mm) : 0.f;
       const float lt = l0 * a0 + l1 * a1;

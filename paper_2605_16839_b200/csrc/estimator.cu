@@ -94,10 +94,14 @@ __global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict
 }
 
 // ---------------------------------------------------------------- a2: block scores
+#ifndef CPA_SCORE_STAGES
+#define CPA_SCORE_STAGES 4
+#endif
 template <int D, int BS>
 struct ScoreCfg {
   static constexpr int kAtoms = D / 64;            // 128-byte swizzle atoms along d
-  static constexpr int kStages = 4;
+  static constexpr int kStages = (D * BS * 2 * CPA_SCORE_STAGES + 2 * 128 * D * 2 + 1280 <= 232448 - 1024)
+                                     ? CPA_SCORE_STAGES : 4;
   static constexpr int kABytes = 128 * D * 2;      // one 128-row qbar tile
   static constexpr int kKBytes = BS * D * 2;       // one K page
   static constexpr int kTmemCols = (2 * BS) <= 32 ? 32 : (2 * BS);
