@@ -150,24 +150,14 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();  // mask_union may be scheduled (it waits for this grid)
-  pdl_wait();     // qbar / row-max init (pool_q) and the appended K pages are complete
 
   // TMA / MMA roles: whole warp runs the loop (warp-uniform values live in uniform registers),
   // one elected lane issues each TMA / tcgen05 instruction.
   if (warp == 0) {  // ---------------- TMA producer
     const int row0 = bg * g.Rpad + rt * 128;
     const int nrows = g.B * g.Gn * g.Rpad;
-    if (elect_one()) {
-      mbar_expect_tx(bar_a, 2 * Cfg::kABytes);
-#pragma unroll
-      for (int a = 0; a < Cfg::kAtoms; ++a) {
-        tma_load_2d(sA_hi + a * 128 * 128, &tm_qbar, bar_a, 64 * a, row0);
-        tma_load_2d(sA_lo + a * 128 * 128, &tm_qbar, bar_a, 64 * a, nrows + row0);
-      }
-    }
-    __syncwarp();
     const uint64_t pol = l2_policy_evict_first();
-    for (int n = 0; n < n_pages; ++n) {
+    auto load_k = [&](int n) {
       const int s = n % Cfg::kStages;
       const int page = __ldg(page_table + (long long)b * g.maxb + j0 + n);
       mbar_wait(empty + s, ((n / Cfg::kStages) & 1) ^ 1);
@@ -179,7 +169,23 @@ __global__ void __launch_bounds__(192, 1)
           tma_load_4d_hint(dst + a * BS * 128, &tm_k, full + s, 64 * a, 0, kvh, page, pol);
       }
       __syncwarp();
+    };
+    // (PDL) the first pages of the ring before waiting for the predecessors, if they are prefix pages
+    // (j < pb): only the chunk's own pages [pb, nkvb) are written by this step's append, and the page
+    // table / earlier pages were complete before the append started (its pdl_wait)
+    int n0 = 0;
+    while (n0 < Cfg::kStages && n0 < n_pages && j0 + n0 < g.pb) load_k(n0++);
+    pdl_wait();  // qbar (pool_q) and the appended K pages are complete
+    if (elect_one()) {
+      mbar_expect_tx(bar_a, 2 * Cfg::kABytes);
+#pragma unroll
+      for (int a = 0; a < Cfg::kAtoms; ++a) {
+        tma_load_2d(sA_hi + a * 128 * 128, &tm_qbar, bar_a, 64 * a, row0);
+        tma_load_2d(sA_lo + a * 128 * 128, &tm_qbar, bar_a, 64 * a, nrows + row0);
+      }
     }
+    __syncwarp();
+    for (int n = n0; n < n_pages; ++n) load_k(n);
   } else if (warp == 1) {  // ---------------- MMA issuer
     constexpr uint32_t idesc = umma_idesc_bf16(128, BS, 0, 0);
     mbar_wait(bar_a, 0);
@@ -217,6 +223,7 @@ __global__ void __launch_bounds__(192, 1)
     const bool valid_row = r < g.R;
     const int i = valid_row ? r % g.nqb : 0;
     const int lim = g.P + min((i + 1) * g.bs, g.C) - 1;  // last absolute key the pooled query sees
+    pdl_wait();  // (PDL) the row-max keys (pool_q) are initialised before this warp touches them
     float row_best = -INFINITY;
     for (int n = 0; n < n_pages; ++n) {
       const int acc = n & 1, j = j0 + n;
