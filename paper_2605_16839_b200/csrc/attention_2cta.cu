@@ -40,12 +40,6 @@ __device__ long long g_trace2[32][2048];
 #define TRACE2(e, i) do {} while (0)
 #endif
 
-// P chunks per warpgroup half-page released separately to the MMA warp (1 = the whole half at once)
-#ifndef CPA_P_CHUNKS
-#define CPA_P_CHUNKS 2
-#endif
-constexpr int kPC = CPA_P_CHUNKS;
-
 template <int BS, bool PERSIST = false>
 struct Attn2Cfg {
   static constexpr int D = 128;
@@ -311,10 +305,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   uint64_t* v_empty = v_full + Cfg::kVStages;       // both: V stage consumed (multicast commit)
   uint64_t* v_ready = v_empty + Cfg::kVStages;      // leader: both V halves converted (4 arrivals)
   uint64_t* s_full = v_ready + Cfg::kVStages;       // both [2]: S^b computed (multicast commit)
-  // leader [2][2][kPC]: P^b columns of WG w written (kPC = 2: each 32-key chunk of a WG's half signals
-  // on its own, so the P.V of its first chunk runs while the WG computes the second)
-  uint64_t* p_full = s_full + 2;
-  uint64_t* pv_done = p_full + 4 * kPC;             // both [2]: last P.V into O_w complete
+  uint64_t* p_full = s_full + 2;                    // leader [2][2]: P^b columns of WG w written
+  uint64_t* pv_done = p_full + 4;                   // both [2]: last P.V into O_w complete
   uint64_t* o_full = pv_done + 2;                   // both: every MMA of the item complete
   uint64_t* o_empty = o_full + 1;                   // leader: epilogue read O (16 warp arrivals)
   uint64_t* stag = o_empty + 1;                     // local [4][2]: WG0 quarter q done with page's max
@@ -343,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       }
       mbar_init(s_full, 1);
       mbar_init(s_full + 1, 1);
-      for (int i = 0; i < 4 * kPC; ++i) mbar_init(p_full + i, 8);  // 4 softmax warps of WG w x 2 CTAs
+      for (int i = 0; i < 4; ++i) mbar_init(p_full + i, 8);  // 4 softmax warps of WG w x 2 CTAs
       mbar_init(pv_done, 1);
       mbar_init(pv_done + 1, 1);
       mbar_init(o_full, 1);
@@ -468,28 +460,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       // O_w += P_w V_n[w-half keys]: WG w's P (keys [w BS/2, (w+1) BS/2) of page n, fp16 packed over its
       // S^b columns) times those V rows; M=256, N=d (64 cols per CTA), K=BS/2
       // commits == false: the caller commits later (P.V(n,1) -> S(n+2) back to back, commits after)
-      // (each P chunk c of the WG's half is waited for separately: P.V of chunk 0 runs while the WG
-      // computes chunk 1)
       auto issue_pv = [&](int n, int w, bool first, bool last, bool commits = true) {
         const uint32_t p_tm = tmem + (n & 1) * 128 + w * (BS / 2);
         const uint32_t o_tm = tmem + 256 + w * 128;
         const uint32_t vb = v_base + (n % Cfg::kVStages) * Cfg::kVHalf + w * (BS / 2) * 128;
-        constexpr int kPer = BS / 32 / kPC;  // K=16 MMAs per P chunk
-#pragma unroll
-        for (int c = 0; c < kPC; ++c) {
-          mbar_wait(p_full + ((n & 1) * 2 + w) * kPC + c, (n >> 1) & 1);
-          tc_fence_after();
-          if (elect_one()) {
-#pragma unroll
-            for (int k2 = 0; k2 < kPer; ++k2) {
-              const int kk = c * kPer + k2;
-              const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
-              mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
-            }
-          }
-          __syncwarp();
-        }
         if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < BS / 32; ++kk) {
+            const uint64_t bd = umma_desc_sw128(vb + kk * 16 * 128, BS * 128, 1024);
+            mma2_ts(o_tm, p_tm + kk * 8, bd, idesc_o, (!first || kk > 0) ? 1u : 0u);
+          }
           if (commits) {
             tc_commit2(pv_done + w);
             if (w == 1) {
@@ -525,7 +505,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           mbar_wait((vf16 ? v_full : v_ready) + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
           if (lane == 0) TRACE2(1, n);
           if (PERSIST && first && i > 0) mbar_wait(o_empty, (i - 1) & 1);  // previous item's O read out of TMEM
+          mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
           if (lane == 0) TRACE2(2, n);
+          tc_fence_after();
           issue_pv(n, 0, first, last);
 #ifndef CPA_NO_MMA_REORDER
           if constexpr (!PERSIST) {
@@ -534,11 +516,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           // (per-unit grid only: in the persistent grid this order broke parity)
           const bool more = n + 2 < G;
           if (more) wait_k(n + 2);
+          mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+          tc_fence_after();
           issue_pv(n, 1, first, last, false);
           if (lane == 0) TRACE2(9, n);
           if (more) issue_s(n + 2);
           pv1_commits(n, last);
           } else {
+          mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+          tc_fence_after();
           issue_pv(n, 1, first, last);
           if (lane == 0) TRACE2(9, n);
           if (n + 2 < G) {
@@ -548,6 +534,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           }
           }
 #else
+          mbar_wait(p_full + 2 * (n & 1) + 1, (n >> 1) & 1);
+          tc_fence_after();
           issue_pv(n, 1, first, last);
           if (lane == 0) TRACE2(9, n);
           if (n + 2 < G) {
@@ -629,8 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
 #ifndef CPA_NO_STAGGER
         if (wg == 0 && lane == 0) mbar_arrive(stag + quarter * 2 + (n & 1));
 #endif
-        if (lane == 0)
-          for (int c = 0; c < kPC; ++c) mbar_arrive_cluster(p_full + ((n & 1) * 2 + wg) * kPC + c, 0);
+        if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
         continue;
 #endif
         uint32_t sv[HC / 32][32];
@@ -672,25 +659,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           if (lane == 0) mbar_arrive(stag + quarter * 2 + (n & 1));
         }
 #endif
-        // rescale O_wg (own rows) after this WG's previous P.V completed, before PV_wg(n) is issued;
-        // not on an item's first page (its P.V overwrites O). Done before the first P chunk is released.
-        if (__any_sync(0xffffffffu, rescale && t > ta)) {
-          mbar_wait(pv_done + wg, (n - 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t o[32];
-            tmem_ld32(o_tm + c0, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
-            tmem_st16(o_tm + c0, *reinterpret_cast<uint32_t(*)[16]>(o));
-            tmem_st16(o_tm + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(o + 16));
-          }
-        }
         // P = exp2(s*sl2 - m): packed f32x2 FFMA; pairs chosen by use_poly_exp on a degree-3
         // polynomial (FMA pipe), the rest on MUFU.EX2; 4 partial f32x2 sums; fp16 pack; stored over S.
-        // Each of the kPC chunks of the WG's keys is released to the MMA warp as soon as it is stored.
         float2 acc[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
         for (int k = 0; k < HC / 32; ++k) {
@@ -709,24 +679,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             pk[q2] = PF16 ? pack_f16x2(e.x, e.y) : pack_bf16x2(e.x, e.y);
           }
           tmem_st16(s_tm + k * 16, pk);
-          constexpr int kStores = HC / 32;  // 16-column P stores per page (2 for bs 128, 1 for bs 64)
-          constexpr int kPerChunk = kStores >= kPC ? kStores / kPC : 1;
-          if ((k + 1) % kPerChunk == 0) {  // chunk k / kPerChunk of this WG's P is in TMEM
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (kStores >= kPC) {
-                mbar_arrive_cluster(p_full + ((n & 1) * 2 + wg) * kPC + k / kPerChunk, 0);
-              } else {  // fewer stores than chunks: the one store releases every chunk
-                for (int c = 0; c < kPC; ++c) mbar_arrive_cluster(p_full + ((n & 1) * 2 + wg) * kPC + c, 0);
-              }
-            }
-          }
         }
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         l_run = l_run * f + ((a01.x + a01.y) + (a23.x + a23.y));
         if (row == 0) TRACE2(12 + 16 * wg, n);
+        // rescale O_wg (own rows) after this WG's previous P.V completed, before PV_wg(n) is issued;
+        // not on an item's first page (its P.V overwrites O)
+        if (__any_sync(0xffffffffu, rescale && t > ta)) {
+          mbar_wait(pv_done + wg, (n - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t o[32];
+            tmem_ld32(o_tm + c0, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * f);
+            tmem_st16(o_tm + c0, *reinterpret_cast<uint32_t(*)[16]>(o));
+            tmem_st16(o_tm + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(o + 16));
+          }
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(p_full + 2 * (n & 1) + wg, 0);
         if (row == 0) TRACE2(6 + 16 * wg, n);
       }
       // ---- item epilogue: merge the two half-softmaxes, O = (O_0 a_0 + O_1 a_1) / (l_0 a_0 + l_1 a_1),
