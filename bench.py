@@ -134,7 +134,7 @@ class ClockSampler:
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_power_cap,power.draw,power.limit")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
@@ -170,8 +170,13 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        num = lambda v: v.replace(".", "", 1).isdigit()
+        pw = [float(s[7]) for s in self.samples if len(s) > 7 and num(s[7])]
+        pl = [float(s[8]) for s in self.samples if len(s) > 8 and num(s[8])]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None,
+                "power_limit_w": max(pl) if pl else None}
 
 
 # ------------------------------------------------------------------------------ CPU oracle (reference arm)

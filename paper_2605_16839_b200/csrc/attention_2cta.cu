@@ -320,6 +320,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   const uint32_t warp = warp_id(), lane = lane_id();
   constexpr uint32_t kConvWarp0 = 8, kTmaWarp = 10, kMmaWarp = 11;
   const bool vf16 = PF16 && (g.flags & (1u << 12)) != 0;  // CPA_F_V_F16: V pages already fp16
+  // fp16 V pool: K and V of a page complete on ONE barrier (k_full), so the MMA warp probes once per page
+  // for its operands (before S(n); P.V(n) is issued after S(n)) instead of twice. A probe costs ~90 cycles
+  // even on a completed phase; measured neutral at 128K (the binding chain is the lagging softmax
+  // warpgroup), kept for the shorter MMA-warp loop.
+#ifndef CPA_NO_KV_BAR
+  const bool kvbar = vf16 && Cfg::kKStages == Cfg::kVStages;
+#else
+  const bool kvbar = false;
+#endif
 
   if (warp == kTmaWarp) {
     if (lane == 0) {
@@ -396,7 +405,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           const int ks = n % Cfg::kKStages, vs = n % Cfg::kVStages;
           mbar_wait(k_empty + ks, ((n / Cfg::kKStages) & 1) ^ 1);
           if (elect_one()) {
-            if (leader) mbar_expect_tx(k_full + ks, 2 * Cfg::kKHalf);
+            if (leader) mbar_expect_tx(k_full + ks, 2 * Cfg::kKHalf + (kvbar ? 2 * Cfg::kVHalf : 0));
             uint8_t* dst = sK + ks * Cfg::kKHalf;
             tma_load_4d_2sm(dst, &tm_k_half, k_full + ks, 0, (int)cta * (BS / 2), kvh, page);
             tma_load_4d_2sm(dst + (BS / 2) * 128, &tm_k_half, k_full + ks, 64, (int)cta * (BS / 2), kvh, page);
@@ -404,7 +413,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           __syncwarp();
           mbar_wait(v_empty + vs, ((n / Cfg::kVStages) & 1) ^ 1);
           if (elect_one()) {
-            if (vf16) {  // fp16 pool: both halves signal the leader's v_full directly (no conversion relay)
+            if (kvbar) {  // fp16 pool, merged barrier: both V halves complete on the page's K barrier
+              tma_load_4d_2sm(sV + vs * Cfg::kVHalf, &tm_v, k_full + ks, 64 * (int)cta, 0, kvh, page);
+            } else if (vf16) {  // fp16 pool: both halves signal the leader's v_full directly (no conversion relay)
               if (leader) mbar_expect_tx(v_full + vs, 2 * Cfg::kVHalf);
               tma_load_4d_2sm(sV + vs * Cfg::kVHalf, &tm_v, v_full + vs, 64 * (int)cta, 0, kvh, page);
             } else {
@@ -502,9 +513,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const int i = it.idx;
         for (int t = it.a; t < it.e; ++t, ++n) {
           const bool first = t == it.a, last = t + 1 == it.e;
-          mbar_wait((vf16 ? v_full : v_ready) + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
-          if (lane == 0) TRACE2(1, n);
           if (PERSIST && first && i > 0) mbar_wait(o_empty, (i - 1) & 1);  // previous item's O read out of TMEM
+          // V(n): with the merged K+V barrier it landed before S(n) was issued (no wait here)
+          if (!kvbar) mbar_wait((vf16 ? v_full : v_ready) + n % Cfg::kVStages, (n / Cfg::kVStages) & 1);
+          if (lane == 0) TRACE2(1, n);
           mbar_wait(p_full + 2 * (n & 1), (n >> 1) & 1);
           if (lane == 0) TRACE2(2, n);
           tc_fence_after();
@@ -608,6 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         // WG1 starts a page when WG0 (same rows, same SMSP) has finished its TMEM load + block max of
         // that page, so one warp's non-MUFU phase overlaps the other's exponentials
         if (wg == 1) mbar_wait(stag + quarter * 2 + (n & 1), (n >> 1) & 1);
+        if (row == 0 && wg == 1) TRACE2(29, n);
 #endif
         mbar_wait(s_full + (n & 1), (n >> 1) & 1);
         if (row == 0) TRACE2(5 + 16 * wg, n);
@@ -657,6 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         if (wg == 0) {
           __syncwarp();
           if (lane == 0) mbar_arrive(stag + quarter * 2 + (n & 1));
+          if (row == 0) TRACE2(13, n);
         }
 #endif
         // P = exp2(s*sl2 - m): packed f32x2 FFMA; pairs chosen by use_poly_exp on a degree-3

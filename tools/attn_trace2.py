@@ -43,6 +43,6 @@ b0 = N // 2
 t0 = int(tr[5, b0])
 for n in range(b0, b0 + 6):
     r = lambda e: int(tr[e, n]) - t0
-    print(f"page {n}: " + " | ".join(
+    print(f"page {n}: wg0 stag_arrived {r(13):6d} wg1 top {r(20):6d} stag_passed {r(29):6d} | " + " | ".join(
         f"wg{w} s_ready {r(5 + 16*w):6d} max {r(11 + 16*w):6d} exp {r(12 + 16*w):6d} arrive {r(6 + 16*w):6d}"
         for w in (0, 1)) + f" || mma: p_seen {r(2):6d} pv_issued {r(9):6d} s(n+2)_issued {r(3):6d}")
