@@ -1,7 +1,8 @@
 """A/B of the chunk step's first half (cpa_prepare_chunk: append + pooled estimator + tables) across
 libcpa builds: CUDA-graph replays, L2 flushed before each, interleaved rounds, median per variant.
 
-  CFG=llama8b_128k KVH=8 ROUNDS=8 REPS=20 python tools/prep_ab.py a.so b.so
+  CFG=llama8b_128k KVH=8 ROUNDS=8 REPS=20 [FLAGSETS=0,32768] python tools/prep_ab.py a.so b.so
+(variants = libs x extra flag sets)
 """
 import os, sys, json, random
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -21,8 +22,14 @@ kc = dev(k[:, :, P:].transpose(0, 2, 1, 3)); vc = dev(v[:, :, P:].transpose(0, 2
 p = cpa.make_params(cfg.batch, KVH * E_, KVH, cfg.head_dim, bs, C, P, alpha=0.06, flags=cpa.F_V_F16)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 libs, graphs, times, ref = {}, {}, {}, None
-for path in sys.argv[1:]:
-    cpa._lib = None; cpa.LIB_PATH = path; libs[path] = cpa.lib()
+base_flags = p.flags
+variants = [(lp, int(f, 0)) for lp in sys.argv[1:] for f in os.environ.get("FLAGSETS", "0").split(",")]
+for path in variants:
+    lp, fl = path
+    p.flags = base_flags | fl
+    if lp not in libs:
+        cpa._lib = None; cpa.LIB_PATH = lp; libs[lp] = cpa.lib()
+    cpa._lib = libs[lp]
     t = cpa.alloc_tables(p); ws = torch.empty(cpa.workspace_bytes(p), dtype=torch.uint8, device="cuda")
     for _ in range(2): cpa.prepare_chunk(p, dq, cache, t, kc, vc, workspace=ws)
     torch.cuda.synchronize()
@@ -43,5 +50,5 @@ for r in range(int(os.environ.get("ROUNDS", "8"))):
             a.record(); g.replay(); b.record(); torch.cuda.synchronize(); times[path].append(a.elapsed_time(b) * 1e3)
 for path in graphs:
     ts = times[path]
-    print(json.dumps({"lib": os.path.basename(path), "cfg": cfg.name, "kv_heads": KVH, "prepare_us_median": round(float(np.median(ts)), 2),
+    print(json.dumps({"lib": os.path.basename(path[0]), "flags": path[1], "cfg": cfg.name, "kv_heads": KVH, "prepare_us_median": round(float(np.median(ts)), 2),
                       "p25": round(float(np.percentile(ts, 25)), 2), "min": round(float(np.min(ts)), 2)}), flush=True)
