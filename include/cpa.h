@@ -87,8 +87,10 @@ enum {
                              Incompatible with CPA_F_P_BF16. The bf16-pool path converts V per page with
                              the same saturating rounding (P.V runs in fp16 either way, K3). */
   CPA_F_NO_PDL = 8192u,   /* ablation: launch the step's kernels without programmatic dependent launch */
-  CPA_F_ATTN_RS = 16384u  /* ablation: row-split 2-CTA attention (one O, three S buffers; d=128, bs=128)
+  CPA_F_ATTN_RS = 16384u, /* ablation: row-split 2-CTA attention (one O, three S buffers; d=128, bs=128)
                              instead of the key-split one (two O accumulators, two S buffers) */
+  CPA_F_ATTN_KS4 = 65536u /* 2-CTA attention with four key slices sharing one running max (one O, three S
+                             buffers; d=128, bs=128, CPA_F_V_F16, per-unit grid) */
 };
 
 typedef struct {

@@ -19,7 +19,7 @@ __all__ = [
     "alloc_tables", "build_tables", "paged_attention", "chunk_step", "append_kv", "prepare_chunk", "last_launch_count",
     "paged_attention_copy", "block_sparse_attention", "expand_tables", "PeerOut", "chunk_step_peer",
     "paged_attention_peer", "peer_barrier", "HostChunkStream",
-    "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "F_NO_PERSIST", "F_PERSIST", "F_V_F16", "F_NO_PDL", "F_ATTN_RS", "EXPORTED_SYMBOLS",
+    "F_SINK", "F_MASK_IN", "F_MASK_OUT", "F_SCORES_OUT", "F_OUT_F32", "F_EXACT_SCORES", "F_P_BF16", "F_NO_2CTA", "F_NO_PERSIST", "F_PERSIST", "F_V_F16", "F_NO_PDL", "F_ATTN_RS", "F_ATTN_KS4", "EXPORTED_SYMBOLS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -27,6 +27,7 @@ LIB_PATH = os.environ.get("CPA_LIB_PATH") or os.path.join(_HERE, "libcpa.so")  #
 
 F_SINK, F_MASK_IN, F_MASK_OUT, F_SCORES_OUT, F_OUT_F32, F_EXACT_SCORES, F_P_BF16, F_NO_2CTA = 1, 2, 4, 8, 16, 32, 256, 512
 F_NO_PERSIST, F_PERSIST, F_V_F16, F_NO_PDL, F_ATTN_RS = 1024, 2048, 4096, 8192, 16384
+F_ATTN_KS4 = 65536
 STATUS = ["CPA_OK", "CPA_ERR_NULL", "CPA_ERR_SHAPE", "CPA_ERR_UNSUPPORTED", "CPA_ERR_MISALIGNED",
           "CPA_ERR_ALPHA", "CPA_ERR_WORKSPACE", "CPA_ERR_CAPACITY", "CPA_ERR_CUDA"]
 EXPORTED_SYMBOLS = ["cpa_workspace_bytes", "cpa_build_tables", "cpa_paged_attention", "cpa_chunk_step",

@@ -8,7 +8,8 @@ from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["api.cu", "estimator.cu", "tables.cu", "attention.cu", "attention_2cta.cu", "append.cu", "peer.cu"]
+SOURCES = ["api.cu", "estimator.cu", "tables.cu", "attention.cu", "attention_2cta.cu", "attention_ks4.cu", "append.cu",
+           "peer.cu"]
 LIB = os.path.join(HERE, "libcpa.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

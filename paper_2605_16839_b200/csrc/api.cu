@@ -32,6 +32,9 @@ bool attn_rs_supported(const Geo& g);
 cudaError_t launch_paged_attention_rs(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
                                       const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 int attn_2cta_max_clusters(const Geo& g);
+bool attn_ks4_supported(const Geo& g);
+cudaError_t launch_paged_attention_ks4(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
+                                       const Geo& g, const AttnArgs& a, cudaStream_t st, int* launches);
 cudaError_t launch_paged_attention_2cta(const CUtensorMap& tq, const CUtensorMap& tk_half, const CUtensorMap& tv,
                                         const Geo& g, const AttnArgs& a, const SkSched* sk, cudaStream_t st,
                                         int* launches);
@@ -373,7 +376,8 @@ struct OutSpec {
 struct AttnPlan {
   CUtensorMap tq, tk, tv, tkh;
   AttnArgs a;
-  int kind;  // 0: 1-CTA kernel, 1: 2-CTA per-unit grid, 2: 2-CTA persistent stream-K grid, 3: row-split 2-CTA
+  int kind;  // 0: 1-CTA kernel, 1: 2-CTA per-unit grid, 2: 2-CTA persistent stream-K grid, 3: row-split 2-CTA,
+             // 4: 2-CTA, four key slices with a shared running max (attention_ks4.cu)
   SkSched sk;
 };
 
@@ -419,6 +423,7 @@ int prep_attention(const cpa_params* p, const Geo& g, const void* q, const void*
       ap->kind = 2;
     }
     if (ap->kind == 1 && attn_rs_supported(g) && (p->flags & CPA_F_ATTN_RS)) ap->kind = 3;
+    if (ap->kind == 1 && attn_ks4_supported(g) && (p->flags & CPA_F_ATTN_KS4)) ap->kind = 4;
   }
   return CPA_OK;
 }
@@ -427,6 +432,7 @@ int run_attention(const Geo& g, const AttnPlan& ap, cudaStream_t st) {
   cudaError_t e;
   if (ap.kind == 0) e = launch_paged_attention(ap.tq, ap.tk, ap.tv, g, ap.a, st, &g_launches);
   else if (ap.kind == 3) e = launch_paged_attention_rs(ap.tq, ap.tkh, ap.tv, g, ap.a, st, &g_launches);
+  else if (ap.kind == 4) e = launch_paged_attention_ks4(ap.tq, ap.tkh, ap.tv, g, ap.a, st, &g_launches);
   else e = launch_paged_attention_2cta(ap.tq, ap.tkh, ap.tv, g, ap.a, ap.kind == 2 ? &ap.sk : nullptr, st, &g_launches);
   if (e != cudaSuccess) return cuda_fail(e, "paged_attention");
   return CPA_OK;

@@ -559,3 +559,35 @@ def test_attention_row_split_and_key_split_kernels(flag, C, P, density):
         got = _gpu_attn(case, t)
         ref = O.paged_attention(q, k, v, P, bs, ip, ix)
         assert rel_err(got, ref) <= ATOL_REL, (flag, vf16)
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,C,P,density", [
+    (2, 8, 2, 256, 8 * 128, 0.05),   # sparse prefix, two q-tiles
+    (2, 8, 2, 200, 384, 1.0),        # full tables, partial second q-tile
+    (1, 8, 2, 130, 1024, 0.3),       # one token past a q-tile
+    (1, 16, 2, 384, 2048, 0.5),      # E = 8: four head pairs per group
+    (1, 4, 2, 1, 640, 0.4),          # single query token
+    (1, 4, 2, 128, 0, 1.0),          # first chunk: only diagonal pages
+])
+def test_attention_four_slice_kernel(B, Hq, Hkv, C, P, density):
+    """CPA_F_ATTN_KS4 (attention_ks4.cu: 16 softmax warps, four key slices sharing one running max,
+    one O, three S buffers) against the oracle on random tables and on the dense table (NULL), fp16 V
+    pool; and against the key-split kernel on the same inputs."""
+    d, bs = 128, 128
+    q, k, v = random_qkv(B, Hq, Hkv, d, C, P + C, seed=C + P + Hq)
+    case = Case(q, k, v, P, bs, seed=9, flags=cpa.F_V_F16 | cpa.F_ATTN_KS4)
+    case.cache = cpa.PagedKVCache(case.cache.k_pages, case.cache.v_pages.half(), case.cache.page_table)
+    nqb, nkvb, pb, _ = O.geometry(C, P, bs)
+    M = random_block_mask(B, Hq, nqb, nkvb, density, seed=C + 1)
+    for i in range(nqb):
+        M[:, :, i, pb + i + 1:] = False
+        M[:, :, i, pb:pb + i + 1] = True
+    ip, ix = O.tables_from_mask(M, case.E, pb)
+    t = cpa.BlockTables(torch.from_numpy(ip).cuda(), torch.from_numpy(ix).cuda())
+    got = _gpu_attn(case, t)
+    assert rel_err(got, O.paged_attention(q, k, v, P, bs, ip, ix)) <= ATOL_REL
+    dense = _gpu_attn(case, None)
+    assert rel_err(dense, O.dense_causal_attention(q, k, v, P)) <= ATOL_REL
+    case.params.flags &= ~cpa.F_ATTN_KS4
+    ks2 = _gpu_attn(case, t)
+    assert rel_err(got, ks2) <= 5e-3
