@@ -473,13 +473,14 @@ def run_gpu(args):
         torch.cuda.synchronize()
         step = graph.replay
 
-    def timed(fn, iters, warm, inner=None, ev=None):
+    def timed(fn, iters, warm, inner=None, ev=None, flush_l2=True):
         for _ in range(warm):
             fn()
         torch.cuda.synchronize()
         ts = []
         for _ in range(iters):
-            flush.zero_()
+            if flush_l2:
+                flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             fn()
@@ -526,6 +527,11 @@ def run_gpu(args):
     t_dense_i = float(np.median(t_dense_l))
     t_step_pair = float(np.median(t_step_l))
     t_append = float(np.mean(timed(lambda: cpa.append_kv(p, kc, vc, cache), reps, 1)))
+    # SURVEY §8(d) protocol extras: the timed steps' spread, and the step with a warm L2 (no flush)
+    t_warm = float(np.median(timed(step, args.steps, 1, flush_l2=False)))
+    step_stats = {"min": round(float(np.min(ts)), 4), "median": round(float(np.median(ts)), 4),
+                  "p90": round(float(np.percentile(ts, 90)), 4), "warm_l2_median": round(t_warm, 4),
+                  "note": "rank 0's K timed steps (L2 flushed before each); warm_l2: K steps without the flush"}
     ip = tables.kv_indptr.cpu().numpy()
     ix = tables.kv_indices.cpu().numpy()[: ip[-1]]
     Gx = hq_l // E_exec
@@ -638,6 +644,7 @@ def run_gpu(args):
                                f"interleaved (step, dense) pairs, median of {reps}: {t_step_pair:.4f} vs "
                                f"{t_dense_i:.4f} ms = {t_dense_i / t_step_pair:.3f}x"),
             "attention_only_speedup": round(t_dense / t_attn, 3),
+            "step_ms_stats": step_stats,
             "stage_ms": {"append": round(t_append, 4), "estimator+tables": round(t_tables, 4),
                          "attention": round(t_attn, 4)},
             "other_v_pool": other_pool,
