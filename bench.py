@@ -222,10 +222,21 @@ def _or_rows(task):
     return len(rows)
 
 
-def oracle_chunk(args, rows_per_group=None, log=None):
+def _pairs(ix, C, P, bs, L):
+    """Causal (query position, key) pairs of one execution group's table (per query head)."""
+    pos = P + np.arange(C)
+    tot = 0
+    for j in ix:
+        lo, hi = int(j) * bs, min(int(j) * bs + bs, L)
+        tot += int(np.clip(pos - lo + 1, 0, hi - lo).sum())
+    return tot
+
+
+def oracle_chunk(args, rows_per_group=None, log=None, one_group=None):
     """Time the oracle on the final chunk of args.config: every group's estimator + tables, then the
     attention rows (all of them, or `rows_per_group` evenly spaced query positions x all heads of each
-    group). Returns (ms/chunk, timed wall ms, description)."""
+    group, or -- one_group = gi -- every row of execution group gi only, scaled to the chunk by the exact
+    causal-pair counts of all groups' tables). Returns (ms/chunk, timed wall ms, description)."""
     import multiprocessing as mp
     cfg = CONFIGS[args.config]
     seed = seed_of(args.config)
@@ -253,15 +264,28 @@ def oracle_chunk(args, rows_per_group=None, log=None):
         t0 = time.perf_counter()
         tabs = pool.map(_or_tables, range(groups), chunksize=1)
         t1 = time.perf_counter()
-        per = max(1, min(64, len(rows_g) // max(1, (2 * cores) // groups + 1)))
-        tasks = [(gi, tabs[gi][0], tabs[gi][1], rows_g[s:s + per]) for gi in range(groups)
+        att_groups = range(groups) if one_group is None else [one_group % groups]
+        per = max(1, min(64, len(rows_g) // max(1, (2 * cores) // len(att_groups) + 1)))
+        tasks = [(gi, tabs[gi][0], tabs[gi][1], rows_g[s:s + per]) for gi in att_groups
                  for s in range(0, len(rows_g), per)]
         done = sum(pool.imap_unordered(_or_rows, tasks, chunksize=1))
         t2 = time.perf_counter()
     n_timed = done
     t_est, t_att = (t1 - t0) * 1e3, (t2 - t1) * 1e3
-    ms = t_est + t_att * (n_total / n_timed)
-    if n_timed == n_total:
+    if one_group is not None:
+        gi = one_group % groups
+        pairs = [_pairs(tabs[g][1], C, P, cfg.block_size, L) for g in range(groups)]
+        ratio = sum(pairs) / pairs[gi]
+        ms = t_est + t_att * ratio
+        desc = (f"estimator + tables of all {groups} execution groups (complete, {t_est:.0f} ms) + attention for "
+                f"every row of execution group {gi} ({n_timed} (b, p, h) rows, {t_att:.0f} ms), scaled to the chunk "
+                f"by the exact causal-pair count of all groups' tables (x{ratio:.3f}; groups differ only in "
+                f"needle placement); fp64 numpy oracle, {cores} worker processes")
+    else:
+        ms = t_est + t_att * (n_total / n_timed)
+    if one_group is not None:
+        pass
+    elif n_timed == n_total:
         desc = (f"whole {cfg.name} final chunk: estimator + tables of all {groups} execution groups and "
                 f"attention for all {n_total} (b, p, h) query rows, fp64 numpy oracle, {cores} worker processes")
     else:
@@ -280,13 +304,15 @@ def run_reference(args):
         return
     log = lambda m: print(m, file=sys.stderr, flush=True)
     vals, walls = [], []
+    whole = args.oracle_rows_per_group is None and args.ref_whole_chunk
+    per_group = args.oracle_rows_per_group is None and not args.ref_whole_chunk
     n_steps = 1 if args.oracle_rows_per_group is None else max(1, args.steps)
-    for _ in range(n_steps):
-        ms, wall, desc, cores = oracle_chunk(args, args.oracle_rows_per_group, log)
+    for st in range(n_steps):
+        ms, wall, desc, cores = oracle_chunk(args, args.oracle_rows_per_group, log,
+                                             one_group=st if per_group else None)
         vals.append(ms)
         walls.append(wall)
     val = float(np.mean(vals))
-    whole = args.oracle_rows_per_group is None
     out = {"impl": "reference", "metric": METRIC, "value": round(val, 2), "unit": UNIT, "n_gpus": args.gpus,
            "steps": n_steps, "warmup": 0, "ms_per_step": round(val, 2), "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -296,7 +322,11 @@ def run_reference(args):
            "e2e": {"value": round(val, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "note": ("steps = whole chunks actually timed (one chunk of the oracle takes minutes on the host "
                     "cores, so --steps/--warmup are not repeated); warm-up = input generation + worker start-up"
-                    if whole else "bounded sample per step, extrapolated to ms/chunk (see cpu_baseline.sample)")}
+                    if whole else
+                    ("one step = the whole estimator + every attention row of one execution group, scaled to the "
+                     "chunk by exact pair counts (--ref-whole-chunk times the whole chunk: r02a measured 360 s "
+                     "for 128K on 16 cores); --steps/--warmup are not repeated"
+                     if per_group else "bounded sample per step, extrapolated to ms/chunk (see cpu_baseline.sample)"))}
     print(json.dumps(out), flush=True)
 
 
@@ -713,6 +743,8 @@ def main():
     ap.add_argument("--variant", default="base", choices=["base", "qdiverse"],
                     help="workload variant (synth/workload.py; qdiverse: union density grows with chunk size)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg (sweeps)")
+    ap.add_argument("--ref-whole-chunk", action="store_true",
+                    help="reference arm: time the oracle on the whole chunk (minutes) instead of one execution group")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
