@@ -478,6 +478,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     }
   } else if (warp >= kConvWarp0) {  // --------------------------------------- V bf16 -> fp16
     const int ct = (warp - kConvWarp0) * 32 + lane;
+#ifdef CPA_TRACE
+    // trace builds, fp16 pool: the idle converter warps observe the tensor-pipe completions of cluster 0
+    // (S(n) landed; P.V(n,0) done; P.V(n,1) + S(n+2) done; K(n) landed) for tools/attn_trace2.py
+    if (vf16 && !PERSIST && blockIdx.x == 0 && lane == 0) {
+      for (int n = 0; n < G; ++n) {
+        if (warp == kConvWarp0) {
+          mbar_wait(s_full + (n & 1), (n >> 1) & 1);
+          TRACE2(14, n);
+          mbar_wait(pv_done, n & 1);
+          TRACE2(15, n);
+        } else {
+          mbar_wait(k_full + n % Cfg::kKStages, (n / Cfg::kKStages) & 1);
+          TRACE2(31, n);
+          mbar_wait(pv_done + 1, n & 1);
+          TRACE2(30, n);
+        }
+      }
+    }
+#endif
     for (int n = 0; n < (vf16 ? 0 : G); ++n) {  // fp16 pool: nothing to convert or relay
       const int vs = n % Cfg::kVStages;
       mbar_wait(v_full + vs, (n / Cfg::kVStages) & 1);
@@ -550,9 +569,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         continue;
 #endif
         uint32_t sv[HC / 32][32];
+#ifndef CPA_EXP_NO_TMEM
 #pragma unroll
         for (int k = 0; k < HC / 32; ++k) tmem_ld32(s_tm + k * 32, sv[k]);
         tmem_wait_ld();
+#else  // A/B only (wrong results): the softmax math on register values, no TMEM traffic
+#pragma unroll
+        for (int k = 0; k < HC / 32; ++k)
+#pragma unroll
+          for (int c = 0; c < 32; ++c) sv[k][c] = __float_as_uint((float)((lane + c + n) & 7));
+#endif
         if (t >= nd) {  // block crosses the causal diagonal of this tile: mask in absolute positions
           const int j = args.indptr != nullptr ? __ldg(args.indices + st + t) : t;
           const int tbase = j * g.bs + wg * HC;
@@ -597,6 +623,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int q2 = 0; q2 < 16; ++q2) {
+#ifdef CPA_EXP_TMEM_ONLY  // A/B only (wrong results): TMEM load + store of every page, no softmax math
+            pk[q2] = sv[k][2 * q2] ^ sv[k][2 * q2 + 1];
+            continue;
+#endif
             float2 x = ffma2(make_float2(__uint_as_float(sv[k][2 * q2]), __uint_as_float(sv[k][2 * q2 + 1])), sl2, -m_use);
             float2 e;
             if (PF16 && use_poly_exp(q2)) {
@@ -608,7 +638,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
             acc[q2 & 3] = fadd2(acc[q2 & 3], e);
             pk[q2] = PF16 ? pack_f16x2(e.x, e.y) : pack_bf16x2(e.x, e.y);
           }
+#ifndef CPA_EXP_NO_TMEM
           tmem_st16(s_tm + k * 16, pk);
+#else
+          if (pk[0] == 0x12345u && pk[15] == 0x6789u) tmem_st16(s_tm + k * 16, pk);  // keep the math live
+#endif
         }
         const float2 a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
         l_run = l_run * f + ((a01.x + a01.y) + (a23.x + a23.y));

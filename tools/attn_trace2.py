@@ -46,3 +46,11 @@ for n in range(b0, b0 + 6):
     print(f"page {n}: wg0 stag_arrived {r(13):6d} wg1 top {r(20):6d} stag_passed {r(29):6d} | " + " | ".join(
         f"wg{w} s_ready {r(5 + 16*w):6d} max {r(11 + 16*w):6d} exp {r(12 + 16*w):6d} arrive {r(6 + 16*w):6d}"
         for w in (0, 1)) + f" || mma: p_seen {r(2):6d} pv_issued {r(9):6d} s(n+2)_issued {r(3):6d}")
+
+# tensor-pipe completions observed by the idle converter warps (fp16 pool): per page, cycles from
+# WG0's s_ready of that page
+print("completions (relative to page 165's WG0 s_ready):")
+for n in range(b0, b0 + 6):
+    r = lambda e: int(tr[e, n]) - t0
+    print(f"page {n}: K landed {r(31):6d} | S(n) done {r(14):6d} | PV(n,0) done {r(15):6d} | PV(n,1)+S(n+2) done {r(30):6d}"
+          f" || mma: p_seen {r(2):6d} pv1_issued {r(9):6d} s(n+2)_issued {r(3):6d} | wg1 P arrive {r(22):6d}")
