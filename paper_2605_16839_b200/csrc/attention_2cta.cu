@@ -269,15 +269,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       fence_barrier_init();
     }
     __syncwarp();
-    pdl_wait();  // tables (mask_union) complete; the other threads wait at the cluster barrier below
-    if constexpr (!PERSIST) {  // one cluster = one whole unit (its table prefix found by the whole warp)
-      int s, n, nd;
-      unit_table_warp(g, args, cl, &s, &n, &nd);
-      if (lane == 0) {
-        single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd;
-        *total_s = n;
-      }
-    } else if (lane == 0) {  // stream-K: share cl of every segment
+    if constexpr (PERSIST) pdl_wait();  // tables complete; the other threads wait at the cluster barrier below
+    if constexpr (PERSIST) {
+      if (lane == 0) {  // stream-K: share cl of every segment
       int total = 0;
       for (int s = 0; s < sk.segments; ++s) {
         int lo, hi;
@@ -285,12 +279,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         total += hi - lo;
       }
       *total_s = total;
+      }
     }
   }
   if (warp == kMmaWarp) tmem_alloc2<512>(tmem_slot);
   tc_fence_before();
   cluster_sync();  // peer barriers initialised, TMEM allocated in both CTAs
   tc_fence_after();
+  if constexpr (!PERSIST) {
+    // one cluster = one whole unit. Its Q tile does not depend on the predecessor kernels (only the
+    // tables do), so it is requested before the PDL wait and the table lookup, overlapping their latency
+    if (warp == kTmaWarp) {
+      const Unit uc = unit_coords(g, cl);
+      if (elect_one()) {
+        if (leader) mbar_expect_tx(q_full, 2 * Cfg::kQBytes);
+        const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;
+        tma_load_4d_2sm(sQ, &tm_q, q_full, 0, h, uc.qt * 128, uc.b);
+        tma_load_4d_2sm(sQ + 128 * 128, &tm_q, q_full, 64, h, uc.qt * 128, uc.b);
+      }
+      __syncwarp();
+      pdl_wait();  // tables complete
+      int s, n, nd;
+      unit_table_warp(g, args, cl, &s, &n, &nd);  // the unit's visible table prefix (whole warp)
+      if (lane == 0) {
+        single_s[0] = cl; single_s[1] = s; single_s[2] = n; single_s[3] = nd;
+        *total_s = n;
+      }
+      // an empty unit: its Q tile must land before the CTA may exit
+      if (n == 0 && leader) mbar_wait(q_full, 0);
+    }
+    __syncthreads();  // single_s / total_s published to the CTA
+  }
   pdl_wait();  // (PDL) every thread: the predecessor's writes (tables) are visible before any access
   const uint32_t tmem = *tmem_slot;
   const int G = *total_s;  // pages this cluster processes (all items)
@@ -305,14 +324,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const int h = uc.grp * g.E + uc.hp * 2 + (int)cta;
         const int kvh = group_kv_head(g, uc.grp);
         const int qb = PERSIST ? (i & 1) : 0;
-        if (PERSIST) mbar_wait(q_empty + qb, ((i >> 1) & 1) ^ 1);
-        if (elect_one()) {
-          if (leader) mbar_expect_tx(q_full + qb, 2 * Cfg::kQBytes);
-          uint8_t* dq = sQ + qb * Cfg::kQBytes;
-          tma_load_4d_2sm(dq, &tm_q, q_full + qb, 0, h, uc.qt * 128, uc.b);
-          tma_load_4d_2sm(dq + 128 * 128, &tm_q, q_full + qb, 64, h, uc.qt * 128, uc.b);
+        if constexpr (PERSIST) {  // (per-unit grid: requested in the prologue)
+          mbar_wait(q_empty + qb, ((i >> 1) & 1) ^ 1);
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(q_full + qb, 2 * Cfg::kQBytes);
+            uint8_t* dq = sQ + qb * Cfg::kQBytes;
+            tma_load_4d_2sm(dq, &tm_q, q_full + qb, 0, h, uc.qt * 128, uc.b);
+            tma_load_4d_2sm(dq + 128 * 128, &tm_q, q_full + qb, 64, h, uc.qt * 128, uc.b);
+          }
+          __syncwarp();
         }
-        __syncwarp();
         const int32_t* ptab = args.page_table + (long long)uc.b * g.maxb;
         const int st = it.start;
         for (int t = it.a; t < it.e; ++t, ++n) {

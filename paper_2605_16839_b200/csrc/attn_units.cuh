@@ -88,6 +88,21 @@ __device__ __forceinline__ void unit_table_warp(const Geo& g, const AttnArgs& ar
   const int r = c.b * g.Gn + c.grp;
   const int s = __ldg(args.indptr + r), len = __ldg(args.indptr + r + 1) - s;
   *start = s;
+  // Fast path: a row ending with exactly the chunk's blocks pb .. nkvb-1 (always so on the estimator
+  // path: they are forced) has both counts in closed form (jmax >= pb, jfull >= pb - 1).
+  // Checked with two parallel loads (first and last tail entry; the row is strictly ascending), since a
+  // caller's MASK_IN tables may lack chunk blocks; otherwise the 32-ary searches.
+  const int nch = g.nkvb - g.pb;
+  if (nch > 0 && len >= nch) {
+    const int v = lane_id() < 2 ? __ldg(args.indices + s + (lane_id() == 0 ? len - nch : len - 1)) : 0;
+    const int first = __shfl_sync(0xffffffffu, v, 0), last = __shfl_sync(0xffffffffu, v, 1);
+    if (first == g.pb && last == g.nkvb - 1) {
+      const int prefix = len - nch;
+      *n = prefix + (jmax - g.pb + 1);
+      *nd = min(*n, prefix + max(0, jfull - g.pb + 1));
+      return;
+    }
+  }
   *n = warp_count_le(args.indices + s, len, jmax);
   *nd = warp_count_le(args.indices + s, *n, jfull);
 }
