@@ -417,7 +417,7 @@ def run_gpu(args):
     seed = seed_of(args.config)
     P, C, L = cfg.chunk_geometry()
     bs, d, E = cfg.block_size, cfg.head_dim, cfg.group_size
-    from paper_2605_16839_b200.shard import allgather_heads, head_shard
+    from paper_2605_16839_b200.shard import allgather_heads, head_shard, heads_view
     kvh, qh = head_shard(cfg.num_q_heads, cfg.num_kv_heads, world, rank)
     hkv_l, hq_l = len(kvh), len(qh)
     k, v = make_kv(cfg, seed, args.rho, kv_heads=kvh, variant=args.variant)
@@ -453,6 +453,7 @@ def run_gpu(args):
     # rank's symmetric-memory buffer + a signal barrier, cpa_chunk_step_peer); NCCL all-gather after a
     # local step is the baseline (--collective nccl) and the fallback if symmetric memory is unavailable.
     peers = None
+    peer_check = None
     full_shape = (cfg.batch, C, cfg.num_q_heads, d)
     if (world > 1 or force_peer) and not one_dev and args.collective == "peer":
         try:
@@ -461,6 +462,35 @@ def run_gpu(args):
             config["parallelism"] = (f"kv-group shard x{world} + nccl all-gather (fallback: symmetric memory "
                                      f"unavailable: {type(ex).__name__}: {ex})")[:240]
             config["launch"] = "direct"
+    if peers is not None:
+        # validate the fused path once against the local step + NCCL all-gather before timing it: a rank
+        # whose gathered buffer differs, or a barrier timeout, switches every rank to the NCCL baseline
+        # (recorded in `parallelism`) instead of losing the run
+        why = ""
+        try:
+            cpa.chunk_step_peer(p, dq, cache, tables, peers, kc, vc, workspace=ws)
+            torch.cuda.synchronize()
+            st_ = int(peers.dev_status.item())
+            if st_ != 0:
+                why = f"peer barrier timed out waiting for rank {st_ - 1}"
+            else:
+                cpa.chunk_step(p, dq, cache, tables, o, kc, vc, workspace=ws)
+                allgather_heads(o, o_all)
+                torch.cuda.synchronize()
+                if not torch.equal(heads_view(o_all), o_gathered):
+                    why = "fused all-gather output differs from the NCCL all-gather"
+        except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+            why = f"{type(ex).__name__}: {ex}"
+        ok = torch.tensor([0 if why else 1], dtype=torch.int32, device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            print(f"[bench] rank {rank}: fused peer path failed validation ({why or 'another rank'}); "
+                  f"using NCCL all-gather", file=sys.stderr, flush=True)
+            peers = None
+            config["parallelism"] = (f"kv-group shard x{world} + nccl all-gather (fallback: fused peer path "
+                                     f"failed validation: {why or 'on another rank'})")[:240]
+            config["launch"] = "direct"
+        peer_check = "fused all-gather bit-equal to local step + NCCL all-gather" if peers is not None else why
     use_graph = config["launch"].startswith("CUDA graph")
 
     def step():
@@ -691,6 +721,7 @@ def run_gpu(args):
                     "bytes_note": "per rank" if world > 1 else "whole job"},
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
+            **({"peer_check": peer_check} if peer_check is not None else {}),
             "paper_context": "2.72x attention speedup at 128K on 2xH200 (TP=2, B=8, chunk 1024; PAPER.md:612, 620)",
         }
         print(json.dumps(out), flush=True)

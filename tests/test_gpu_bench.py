@@ -49,3 +49,23 @@ def test_bench_two_ranks_one_device():
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["config"]["parallelism"].startswith("kv-group shard x2")
     assert d["roofline"]["frac"] > 0 and d["cpu_baseline"]["value"] > 0
+
+
+def test_bench_fused_peer_path_validated():
+    """The fused peer all-gather path of an N>1 run, exercised on one GPU with a 1-rank NCCL group
+    (CPA_BENCH_PEER_W1 under torchrun): torch symmetric memory, cpa_chunk_step_peer, the pre-timing
+    check against the local step + NCCL all-gather, and the CUDA-graph-replayed timed step."""
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e["CPA_BENCH_PEER_W1"] = "1"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"), "--gpus", "1", "--config",
+           "llama8b_32k", "--steps", "2", "--warmup", "3", "--no-cpu"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=e)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert d["peer_check"].startswith("fused all-gather bit-equal"), d.get("peer_check")
+    assert d["config"]["launch"].startswith("CUDA graph") and d["value"] > 0
