@@ -14,16 +14,18 @@
 namespace cpa {
 
 // ---------------------------------------------------------------- a1: pool Q
-// grid (nqb + 1, B, ceil(Hq*d/512)), block 1024 threads = 16 token parts x 64 slab threads; a slab
-// thread owns 8 consecutive elements (one uint4) of a 512-element slice of [Hq*d]; each part sums
+// grid (nqb + 1, B, ceil(Hq*d/128)), block 256 threads = 16 token parts x 16 slab threads; a slab
+// thread owns 8 consecutive elements (one uint4) of a 128-element slice of [Hq*d] (narrow slices: at one
+// KV group per GPU, Hq*d = 512, 512-element slices gave only nqb + 1 CTAs); each part sums
 // 1/16 of the q-block's tokens with all its loads in flight at once (8 for bs = 128), the parts are
 // combined in shared memory. Blocks x = nqb zero the padding rows [R, Rpad) of qbar (padded MMA rows
 // must be finite). qbar: [2][B*Gn*Rpad][d] bf16 (hi rows, then lo rows).
 constexpr int kPoolParts = 16;
-__global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
+constexpr int kSlabT = 16;  // slab threads per CTA (kSlabT * 8 elements of [Hq*d])
+__global__ void __launch_bounds__(kPoolParts * kSlabT) k_pool_q(const __nv_bfloat16* __restrict__ q, Geo g,
                                                  __nv_bfloat16* __restrict__ qbar, int* __restrict__ mstar_key,
                                                  unsigned* __restrict__ tables_done) {
-  __shared__ float part[kPoolParts - 1][64][9];
+  __shared__ float part[kPoolParts - 1][kSlabT][9];
   const int i = blockIdx.x, b = blockIdx.y;
   pdl_trigger();  // block_scores may start its prologue; it waits for this grid before reading qbar
   if (i == 0 && b == 0 && blockIdx.z == 0 && threadIdx.x == 0) *tables_done = 0u;  // k_mask_union's counter
@@ -40,8 +42,8 @@ __global__ void __launch_bounds__(1024) k_pool_q(const __nv_bfloat16* __restrict
     pdl_wait();  // this grid completes only after its predecessor (the append of the chunk's K/V)
     return;
   }
-  const int st = threadIdx.x & 63, pt = threadIdx.x >> 6;
-  const int x0 = (blockIdx.z * 64 + st) * 8;  // element offset in [0, Hq*d)
+  const int st = threadIdx.x % kSlabT, pt = threadIdx.x / kSlabT;
+  const int x0 = (blockIdx.z * kSlabT + st) * 8;  // element offset in [0, Hq*d)
   const bool active = x0 < g.Hq * g.d;         // last slab may be partial (Hq*d % 512 != 0)
   const int p0 = i * g.bs, p1 = min(p0 + g.bs, g.C);
   const int nq = (p1 - p0 + kPoolParts - 1) / kPoolParts;
@@ -489,7 +491,8 @@ cudaError_t launch_pool_q(const __nv_bfloat16* q, const Geo& g, __nv_bfloat16* q
   // x = nqb: padding blocks (they return at once when Rpad == R). PDL only right after k_append (whose
   // pdl_wait orders it after everything before): then q, qbar and the counters are safe to touch early.
   ++*launches;
-  return launch_ex(k_pool_q, dim3(g.nqb + (g.Rpad > g.R ? 1 : 0), g.B, (g.Hq * g.d + 511) / 512), dim3(1024), 0, st,
+  return launch_ex(k_pool_q, dim3(g.nqb + (g.Rpad > g.R ? 1 : 0), g.B, (g.Hq * g.d + kSlabT * 8 - 1) / (kSlabT * 8)),
+                   dim3(kPoolParts * kSlabT), 0, st,
                    after_append && use_pdl(g), q, g, qbar, mstar_key, tables_done);
 }
 
