@@ -473,14 +473,16 @@ def run_gpu(args):
             st_ = int(peers.dev_status.item())
             if st_ != 0:
                 why = f"peer barrier timed out waiting for rank {st_ - 1}"
-            else:
-                cpa.chunk_step(p, dq, cache, tables, o, kc, vc, workspace=ws)
-                allgather_heads(o, o_all)
-                torch.cuda.synchronize()
-                if not torch.equal(heads_view(o_all), o_gathered):
-                    why = "fused all-gather output differs from the NCCL all-gather"
         except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
             why = f"{type(ex).__name__}: {ex}"
+        try:
+            cpa.chunk_step(p, dq, cache, tables, o, kc, vc, workspace=ws)
+        except Exception as ex:  # noqa: BLE001
+            why = why or f"{type(ex).__name__}: {ex}"
+        allgather_heads(o, o_all)  # every rank, whatever happened above (same collective sequence)
+        torch.cuda.synchronize()
+        if not why and not torch.equal(heads_view(o_all), o_gathered):
+            why = "fused all-gather output differs from the NCCL all-gather"
         ok = torch.tensor([0 if why else 1], dtype=torch.int32, device="cuda")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if int(ok.item()) == 0:
